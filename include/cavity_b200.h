@@ -238,21 +238,22 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
 /* ---- block level: one rank's device-resident state ---------------------- */
 typedef struct cav_block cav_block;
 
-/* Everything rank_main derives before its loop (src/runner.cpp:150-182). */
+/* Everything rank_main derives before its loop (src/runner.cpp:150-182):
+ * the block's extent, neighbours, plan, overlap regions and centre owner are
+ * computed from the global grid, the block dims and the rank, exactly as
+ * make_block_map/partition/neighbors do. Local grids keep the global spacing
+ * (src/runner.cpp:19-25). */
 typedef struct {
   int rank, np;
   int gnx, gny, gnz;        /* global interior */
-  int lo[3], hi[3];         /* this block's global extent */
-  int rank_at[6];           /* neighbours, CAV_WALL for walls */
-  int center_owner;         /* rank that owns center_node() */
-  int center_local[3];      /* storage coords of the centre node on the owner */
+  int dims[3];              /* block counts (choose_dims or explicit) */
   int strategy, overlap;
   cav_fluid_params fluid;
-  double dx, dy, dz;        /* global spacing (src/runner.cpp:19-25) */
   double cfl;
   int rescale;
   int corrupt_exchange;     /* ExchangePlan.corrupt_first hook */
   int device;
+  double timeout_ms;        /* device-side wait limit for peers */
 } cav_block_desc;
 
 int cav_block_create(const cav_block_desc* desc, cav_block** out);

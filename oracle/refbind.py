@@ -43,23 +43,7 @@ def default_config(**kw):
     return apply_overrides(cfg, **kw)
 
 
-def apply_overrides(cfg, **kw):
-    for k, v in kw.items():
-        if k == "grid":
-            cfg.nx, cfg.ny, cfg.nz = v
-        elif k == "mode":
-            cfg.mode = A.MODES[v] if isinstance(v, str) else v
-        elif k == "strategy":
-            cfg.strategy = A.STRATEGIES[v] if isinstance(v, str) else v
-        elif k == "dims":
-            for a in range(3):
-                cfg.dims[a] = v[a]
-        elif k in ("rho", "nu", "alpha", "sigma", "u_ref", "kappa", "t_hot", "t_cold", "t_inf",
-                   "length"):
-            setattr(cfg.fluid, k, v)
-        else:
-            setattr(cfg, k, v)
-    return cfg
+apply_overrides = A.apply_overrides
 
 
 def _run(fn, errfn, cfg, collect_fields, collect_history, corrupt=False):

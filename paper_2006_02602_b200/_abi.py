@@ -92,12 +92,10 @@ class CaseResultC(C.Structure):
 
 class BlockDesc(C.Structure):
     _fields_ = [("rank", C.c_int), ("np", C.c_int), ("gnx", C.c_int), ("gny", C.c_int),
-                ("gnz", C.c_int), ("lo", C.c_int * 3), ("hi", C.c_int * 3),
-                ("rank_at", C.c_int * 6), ("center_owner", C.c_int),
-                ("center_local", C.c_int * 3), ("strategy", C.c_int), ("overlap", C.c_int),
-                ("fluid", FluidParams), ("dx", C.c_double), ("dy", C.c_double),
-                ("dz", C.c_double), ("cfl", C.c_double), ("rescale", C.c_int),
-                ("corrupt_exchange", C.c_int), ("device", C.c_int)]
+                ("gnz", C.c_int), ("dims", C.c_int * 3), ("strategy", C.c_int),
+                ("overlap", C.c_int), ("fluid", FluidParams), ("cfl", C.c_double),
+                ("rescale", C.c_int), ("corrupt_exchange", C.c_int), ("device", C.c_int),
+                ("timeout_ms", C.c_double)]
 
 
 class RunIO(C.Structure):
@@ -106,3 +104,32 @@ class RunIO(C.Structure):
                 ("check_iters", C.POINTER(C.c_longlong)), ("n_checks", C.c_longlong),
                 ("err_iteration", C.c_longlong), ("err_kind", C.c_int),
                 ("seconds", C.c_double), ("ledger", Ledger)]
+
+
+def apply_overrides(cfg, **kw):
+    """Set RunConfig fields by name; fluid constants may be given flat
+    (nu=..., t_hot=...), grid as a 3-tuple, mode/strategy as names."""
+    for k, v in kw.items():
+        if k == "grid":
+            cfg.nx, cfg.ny, cfg.nz = v
+        elif k == "mode":
+            cfg.mode = MODES[v] if isinstance(v, str) else v
+        elif k == "strategy":
+            cfg.strategy = STRATEGIES[v] if isinstance(v, str) else v
+        elif k == "dims":
+            for a in range(3):
+                cfg.dims[a] = v[a]
+        elif k == "devices":
+            for a in range(8):
+                cfg.devices[a] = v[a % len(v)]
+        elif k == "gravity":
+            for a in range(3):
+                cfg.fluid.gravity[a] = v[a]
+        elif k in ("rho", "nu", "alpha", "sigma", "u_ref", "kappa", "t_hot", "t_cold", "t_inf",
+                   "length"):
+            setattr(cfg.fluid, k, v)
+        else:
+            if not hasattr(cfg, k):
+                raise AttributeError("RunConfig has no field " + k)
+            setattr(cfg, k, v)
+    return cfg

@@ -1,0 +1,1296 @@
+// block.cu — one rank's device-resident state and its per-iteration pipeline:
+// the B200-native replacement of rank_main's loop body
+// (/root/reference/proj/src/runner.cpp:184-235).
+//
+// Iteration n on rank r (all on the block's stream unless overlapping):
+//   K1 bc        wall ghosts of state A from the lazily shifted interior
+//                (apply_boundary_conditions, src/solver.cpp:158-191)
+//   K2 pack      plan entries of A pushed straight into the neighbours'
+//                receive slabs over NVLink/peer memory, release flag per entry
+//                (exchange_begin, src/exchange.cpp:115-145)
+//   K3 unpack    acquire flag, scatter into A's join ghosts
+//                (exchange_finish, src/exchange.cpp:147-176)
+//   K4 step      fused: residual + [exact norm digits] + Euler update into B
+//                + next-step CFL maxima + non-finite flags + centre pressure
+//                (compute_residual, global_norms, compute_dt, euler_step,
+//                center_pressure_broadcast; src/runner.cpp:196-228)
+//   K6 sync      push (maxima, pc, err) to every rank's slot, wait for all,
+//                fold dt_{n+1} and pc_n (reduce_fixed_order(Min) and
+//                broadcast_double, src/transport.cpp:23-60); replaces barrier()
+// The rescale p -= pc_n is never a separate pass: every consumer of A applies
+// fl(p - pc_{n-1}) when it loads an interior pressure.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "host.hpp"
+#include "ops.hpp"
+#include "status.hpp"
+
+namespace cav {
+
+// ---------------------------------------------------------------------------
+// Fused step, tiled: 32 x TY threads own (i,j) columns of one tile and stream
+// k. Pressure k-2..k+2 and u,v,w,T k-1..k+1 of the own column sit in
+// registers; the in-plane neighbours come from a double-buffered shared-memory
+// plane with a cross-shaped halo (2 for p, 1 for the rest; corners are never
+// read). Next-plane loads are issued before the current plane is computed.
+struct StepArgs {
+  const double* in;
+  double* out;
+  Geo g;
+  cav_stencil_params sp;
+  cav_box box;
+  int kchunk;
+  const IterScalars* sc;
+  Acc* acc;
+  unsigned long long* digits;  // 5*70 for check iterations, else null
+  int cx, cy, cz;              // centre node storage coords on the owner, else -1
+  long long n;
+  int rank;
+};
+
+template <int NT, bool NORMS>
+__device__ __forceinline__ void step_epilogue(const StepArgs& a, double m0, double m1, double m2, unsigned bad,
+                                              unsigned nbad, unsigned long long* sdig) {
+  block_reduce_max3_or<NT>(m0, m1, m2, bad);
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  if (tid == 0) acc_publish(a.acc, m0, m1, m2, bad, a.n + 1, a.rank);
+  if (NORMS) {
+    nbad = __syncthreads_or(nbad);
+    if (tid == 0 && nbad) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
+    for (int x = tid; x < 5 * kDigits; x += NT)
+      if (sdig[x]) atomicAdd(&a.digits[x], sdig[x]);
+  }
+}
+
+template <int TY, bool NORMS>
+__global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
+  constexpr int TX = 32, NT = TX * TY;
+  constexpr int PW = TX + 4, PH = TY + 4, QW = TX + 2, QH = TY + 2;
+  constexpr int PLANE_P = PH * PW, PLANE_Q = QH * QW;
+  constexpr int BUF = PLANE_P + 4 * PLANE_Q;
+  constexpr int NH = 12 * TX + 12 * TY;  // halo elements per plane (p: 4TX+4TY, q: 4*(2TX+2TY))
+  constexpr int NS = (NH + NT - 1) / NT;
+  __shared__ __align__(16) double sm[2 * BUF];
+  __shared__ unsigned long long sdig[NORMS ? 5 * kDigits : 1];
+
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const Geo g = a.g;
+  const int ti0 = a.box.lo[0] + blockIdx.x * TX, tj0 = a.box.lo[1] + blockIdx.y * TY;
+  const int i = ti0 + tx, j = tj0 + ty;
+  const int kb = a.box.lo[2] + blockIdx.z * a.kchunk;
+  const int ke = min(kb + a.kchunk, a.box.hi[2]);
+  const bool active = i < a.box.hi[0] && j < a.box.hi[1];
+  const bool inst = i < g.nx + 4 && j < g.ny + 4;
+  const bool ij_int = i >= 2 && i < g.nx + 2 && j >= 2 && j < g.ny + 2;
+  const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
+  const long long fs = g.fstride;
+  const double pc = a.sc->pc, dt = a.sc->dt;
+  const double* __restrict__ in = a.in;
+  double* __restrict__ out = a.out;
+  const long long col = g.idx(i, j, 0);
+  const int kzl = 2, kzh = g.nz + 2, kst = g.nz + 4;
+
+  if (NORMS) {
+    for (int x = tid; x < 5 * kDigits; x += NT) sdig[x] = 0;
+  }
+
+  // halo slots: (source column pointer, smem offset, shiftable)
+  const double* hsrc[NS];
+  int hdst[NS];
+  bool hsh[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int h = tid + s * NT;
+    hsrc[s] = nullptr;
+    hdst[s] = 0;
+    hsh[s] = false;
+    if (h < NH) {
+      int f, ii, jj, so;
+      if (h < 4 * TX + 4 * TY) {  // pressure, 2-wide cross halo
+        f = 0;
+        if (h < 2 * TX) {
+          const int r = h / TX, c = h % TX;
+          ii = ti0 + c;
+          jj = tj0 - 2 + r;
+          so = r * PW + 2 + c;
+        } else if (h < 4 * TX) {
+          const int e = h - 2 * TX, r = e / TX, c = e % TX;
+          ii = ti0 + c;
+          jj = tj0 + TY + r;
+          so = (TY + 2 + r) * PW + 2 + c;
+        } else if (h < 4 * TX + 2 * TY) {
+          const int e = h - 4 * TX, c = e / TY, r = e % TY;
+          ii = ti0 - 2 + c;
+          jj = tj0 + r;
+          so = (r + 2) * PW + c;
+        } else {
+          const int e = h - 4 * TX - 2 * TY, c = e / TY, r = e % TY;
+          ii = ti0 + TX + c;
+          jj = tj0 + r;
+          so = (r + 2) * PW + TX + 2 + c;
+        }
+      } else {  // u, v, w, T, 1-wide cross halo
+        const int e0 = h - (4 * TX + 4 * TY);
+        f = 1 + e0 / (2 * TX + 2 * TY);
+        const int e = e0 % (2 * TX + 2 * TY);
+        int r, c;
+        if (e < TX) {
+          ii = ti0 + e;
+          jj = tj0 - 1;
+          r = 0;
+          c = 1 + e;
+        } else if (e < 2 * TX) {
+          ii = ti0 + e - TX;
+          jj = tj0 + TY;
+          r = TY + 1;
+          c = 1 + e - TX;
+        } else if (e < 2 * TX + TY) {
+          ii = ti0 - 1;
+          jj = tj0 + e - 2 * TX;
+          r = 1 + e - 2 * TX;
+          c = 0;
+        } else {
+          ii = ti0 + TX;
+          jj = tj0 + e - 2 * TX - TY;
+          r = 1 + e - 2 * TX - TY;
+          c = TX + 1;
+        }
+        so = PLANE_P + (f - 1) * PLANE_Q + r * QW + c;
+      }
+      hdst[s] = so;
+      if (ii >= 0 && ii < g.nx + 4 && jj >= 0 && jj < g.ny + 4) {
+        hsrc[s] = in + f * fs + g.idx(ii, jj, 0);
+        hsh[s] = f == 0 && ii >= 2 && ii < g.nx + 2 && jj >= 2 && jj < g.ny + 2;
+      }
+    }
+  }
+
+  auto ldc = [&](int f, int k) -> double {
+    return (inst && k >= 0 && k < kst) ? in[f * fs + col + k * plane] : 0.0;
+  };
+  auto shift_at = [&](bool ijok, int k) -> double { return (ijok && k >= kzl && k < kzh) ? pc : 0.0; };
+
+  double pm2 = ldc(0, kb - 2) - shift_at(ij_int, kb - 2);
+  double pm1 = ldc(0, kb - 1) - shift_at(ij_int, kb - 1);
+  double p0 = ldc(0, kb) - shift_at(ij_int, kb);
+  double pp1 = ldc(0, kb + 1) - shift_at(ij_int, kb + 1);
+  double pp2 = ldc(0, kb + 2) - shift_at(ij_int, kb + 2);
+  double um1 = ldc(1, kb - 1), u0 = ldc(1, kb), up1 = ldc(1, kb + 1);
+  double vm1 = ldc(2, kb - 1), v0 = ldc(2, kb), vp1 = ldc(2, kb + 1);
+  double wm1 = ldc(3, kb - 1), w0 = ldc(3, kb), wp1 = ldc(3, kb + 1);
+  double tm1 = ldc(4, kb - 1), t0 = ldc(4, kb), tp1 = ldc(4, kb + 1);
+  double hcur[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) hcur[s] = (hsrc[s] && kb < ke) ? hsrc[s][kb * plane] : 0.0;
+
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  unsigned bad = 0, nbad = 0;
+  const double u_ref = a.sp.u_ref;
+
+  for (int k = kb; k < ke; ++k) {
+    const bool more = k + 1 < ke;
+    // issue next-plane loads first; they land while this plane computes
+    const double np3 = more ? ldc(0, k + 3) : 0.0;
+    const double nu2 = more ? ldc(1, k + 2) : 0.0;
+    const double nv2 = more ? ldc(2, k + 2) : 0.0;
+    const double nw2 = more ? ldc(3, k + 2) : 0.0;
+    const double nt2 = more ? ldc(4, k + 2) : 0.0;
+    double hnext[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) hnext[s] = (more && hsrc[s]) ? hsrc[s][(k + 1) * plane] : 0.0;
+
+    double* B = sm + (k & 1) * BUF;
+    B[(ty + 2) * PW + tx + 2] = p0;
+    double* BQ = B + PLANE_P + (ty + 1) * QW + tx + 1;
+    BQ[0] = u0;
+    BQ[PLANE_Q] = v0;
+    BQ[2 * PLANE_Q] = w0;
+    BQ[3 * PLANE_Q] = t0;
+    const bool kint = k >= kzl && k < kzh;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (tid + s * NT < NH) B[hdst[s]] = hcur[s] - ((hsh[s] && kint) ? pc : 0.0);
+    __syncthreads();
+
+    if (active) {
+      const double* BP = B + (ty + 2) * PW + tx + 2;
+      Star st;
+      st.p = p0;
+      st.pxm = BP[-1];
+      st.pxp = BP[1];
+      st.pxm2 = BP[-2];
+      st.pxp2 = BP[2];
+      st.pym = BP[-PW];
+      st.pyp = BP[PW];
+      st.pym2 = BP[-2 * PW];
+      st.pyp2 = BP[2 * PW];
+      st.pzm = pm1;
+      st.pzp = pp1;
+      st.pzm2 = pm2;
+      st.pzp2 = pp2;
+      const double* BU = BQ;
+      st.u = u0;
+      st.uxm = BU[-1];
+      st.uxp = BU[1];
+      st.uym = BU[-QW];
+      st.uyp = BU[QW];
+      st.uzm = um1;
+      st.uzp = up1;
+      const double* BV = BQ + PLANE_Q;
+      st.v = v0;
+      st.vxm = BV[-1];
+      st.vxp = BV[1];
+      st.vym = BV[-QW];
+      st.vyp = BV[QW];
+      st.vzm = vm1;
+      st.vzp = vp1;
+      const double* BW = BQ + 2 * PLANE_Q;
+      st.w = w0;
+      st.wxm = BW[-1];
+      st.wxp = BW[1];
+      st.wym = BW[-QW];
+      st.wyp = BW[QW];
+      st.wzm = wm1;
+      st.wzp = wp1;
+      const double* BT = BQ + 3 * PLANE_Q;
+      st.t = t0;
+      st.txm = BT[-1];
+      st.txp = BT[1];
+      st.tym = BT[-QW];
+      st.typ = BT[QW];
+      st.tzm = tm1;
+      st.tzp = tp1;
+      const Res r = residual_of(st, a.sp);
+      // euler_step: q = q + dt*r (src/solver.cpp:239-246)
+      const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
+                   qt = t0 + dt * r.t;
+      const long long c = col + k * plane;
+      out[c] = qp;
+      out[fs + c] = qu;
+      out[2 * fs + c] = qv;
+      out[3 * fs + c] = qw;
+      out[4 * fs + c] = qt;
+      const Denoms d = cfl_denoms(qu, qv, qw, u_ref);
+      m0 = dmax_d(m0, d.du);
+      m1 = dmax_d(m1, d.dv);
+      m2 = dmax_d(m2, d.dw);
+      bad |= nonfinite(qp) | (nonfinite(qu) << 1) | (nonfinite(qv) << 2) | (nonfinite(qw) << 3) |
+             (nonfinite(qt) << 4);
+      if (i == a.cx && j == a.cy && k == a.cz) a.acc->pc_local = qp;
+      if (NORMS) {
+        const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
+#pragma unroll
+        for (int v = 0; v < 5; ++v) {
+          if (nonfinite(rr[v])) nbad = 1;
+          else add_term_digits(sdig + v * kDigits, rr[v]);
+        }
+      }
+    }
+
+    pm2 = pm1;
+    pm1 = p0;
+    p0 = pp1;
+    pp1 = pp2;
+    pp2 = np3 - shift_at(ij_int, k + 3);
+    um1 = u0;
+    u0 = up1;
+    up1 = nu2;
+    vm1 = v0;
+    v0 = vp1;
+    vp1 = nv2;
+    wm1 = w0;
+    w0 = wp1;
+    wp1 = nw2;
+    tm1 = t0;
+    t0 = tp1;
+    tp1 = nt2;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) hcur[s] = hnext[s];
+  }
+  __syncthreads();
+  step_epilogue<NT, NORMS>(a, m0, m1, m2, bad, nbad, sdig);
+}
+
+// Fused step, pointwise: one thread per cell of up to six boxes (the overlap
+// shells of src/overlap.cpp:13-28), neighbours straight from L1/L2.
+struct ShellArgs {
+  StepArgs s;
+  int nbox;
+  cav_box box[6];
+  long long start[7];
+};
+
+constexpr int kShellThreads = 256;
+
+template <bool NORMS>
+__global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a) {
+  __shared__ unsigned long long sdig[NORMS ? 5 * kDigits : 1];
+  const StepArgs& s = a.s;
+  if (NORMS) {
+    for (int x = threadIdx.x; x < 5 * kDigits; x += kShellThreads) sdig[x] = 0;
+    __syncthreads();
+  }
+  const long long q = blockIdx.x * static_cast<long long>(kShellThreads) + threadIdx.x;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  unsigned bad = 0, nbad = 0;
+  if (q < a.start[a.nbox]) {
+    int b = 0;
+    while (q >= a.start[b + 1]) ++b;
+    const cav_box& bx = a.box[b];
+    const long long e = q - a.start[b];
+    const int w = bx.hi[0] - bx.lo[0], h = bx.hi[1] - bx.lo[1];
+    const int i = bx.lo[0] + static_cast<int>(e % w);
+    const int j = bx.lo[1] + static_cast<int>((e / w) % h);
+    const int k = bx.lo[2] + static_cast<int>(e / (static_cast<long long>(w) * h));
+    const Geo& g = s.g;
+    const long long fs = g.fstride;
+    const double pc = s.sc->pc, dt = s.sc->dt;
+    const Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
+    const Res r = residual_of(st, s.sp);
+    const double qp = st.p + dt * r.p, qu = st.u + dt * r.u, qv = st.v + dt * r.v, qw = st.w + dt * r.w,
+                 qt = st.t + dt * r.t;
+    const long long c = g.idx(i, j, k);
+    s.out[c] = qp;
+    s.out[fs + c] = qu;
+    s.out[2 * fs + c] = qv;
+    s.out[3 * fs + c] = qw;
+    s.out[4 * fs + c] = qt;
+    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref);
+    m0 = d.du;
+    m1 = d.dv;
+    m2 = d.dw;
+    bad = nonfinite(qp) | (nonfinite(qu) << 1) | (nonfinite(qv) << 2) | (nonfinite(qw) << 3) |
+          (nonfinite(qt) << 4);
+    if (i == s.cx && j == s.cy && k == s.cz) s.acc->pc_local = qp;
+    if (NORMS) {
+      const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        if (nonfinite(rr[v])) nbad = 1;
+        else add_term_digits(sdig + v * kDigits, rr[v]);
+      }
+    }
+  }
+  if (NORMS) __syncthreads();
+  step_epilogue<kShellThreads, NORMS>(s, m0, m1, m2, bad, nbad, sdig);
+}
+
+// ---------------------------------------------------------------------------
+// Halo exchange: one descriptor per plan entry (= one reference message).
+struct MsgDesc {
+  int face;
+  int nvars;
+  int var[5];
+  long long voff[6];  // payload offset of each variable's box (copy_box_to order)
+  cav_box box[5];     // pack: face_interior_box; unpack: face_ghost_box
+  long long scalars;
+  double* slab;               // pack: receiver's slab (parity 0); unpack: own slab
+  unsigned long long* flag;   // pack: receiver's flag; unpack: own flag
+  unsigned* counter;          // pack: CTA completion counter
+  int peer;
+};
+
+struct XArgs {
+  double* state;
+  Geo g;
+  const MsgDesc* msg;
+  long long n;
+  const IterScalars* sc;
+  int corrupt;
+  unsigned long long timeout_ns;
+  unsigned long long* timeout_flag;
+  int rank;
+};
+
+constexpr int kXThreads = 256, kXItems = 4;
+
+__device__ __forceinline__ void msg_locate(const MsgDesc& m, long long q, int& v, int& i, int& j, int& k) {
+  int s = 0;
+  while (s + 1 < m.nvars && q >= m.voff[s + 1]) ++s;
+  const cav_box& b = m.box[s];
+  const long long e = q - m.voff[s];
+  const int w = b.hi[0] - b.lo[0], h = b.hi[1] - b.lo[1];
+  i = b.lo[0] + static_cast<int>(e % w);
+  j = b.lo[1] + static_cast<int>((e / w) % h);
+  k = b.lo[2] + static_cast<int>(e / (static_cast<long long>(w) * h));
+  v = m.var[s];
+}
+
+__global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
+  const MsgDesc& m = a.msg[blockIdx.y];
+  const double pc = a.sc->pc;
+  double* dst = m.slab + (a.n & 1) * m.scalars;
+  const long long base = static_cast<long long>(blockIdx.x) * kXThreads * kXItems;
+#pragma unroll
+  for (int it = 0; it < kXItems; ++it) {
+    const long long q = base + it * kXThreads + threadIdx.x;
+    if (q < m.scalars) {
+      int v, i, j, k;
+      msg_locate(m, q, v, i, j, k);
+      double x = a.state[v * a.g.fstride + a.g.idx(i, j, k)];
+      if (v == 0) x = x - pc;  // sender's interior is the rescaled field
+      dst[q] = x;              // remote store into the neighbour's slab
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned done = atomicAdd(m.counter, 1u);
+    if (done == gridDim.x - 1) {
+      *m.counter = 0;
+      __threadfence_system();
+      st_release_sys(m.flag, static_cast<unsigned long long>(a.n));
+    }
+  }
+}
+
+// Waits for every receive flag of iteration n (acquire, system scope). One
+// small CTA, so a peer's pack can always find an SM even when several ranks
+// share one GPU (the in-process test topology).
+__global__ void __launch_bounds__(32) k_wait_flags(const XArgs a, int nmsg) {
+  for (int m = threadIdx.x; m < nmsg; m += 32) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(a.msg[m].flag) < static_cast<unsigned long long>(a.n)) {
+      if (globaltimer_ns() - t0 > a.timeout_ns) {
+        atomicMin(a.timeout_flag, err_code(a.n, a.rank, 8 + a.msg[m].face));
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __threadfence();
+}
+
+__global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
+  const MsgDesc& m = a.msg[blockIdx.y];
+  const long long base = static_cast<long long>(blockIdx.x) * kXThreads * kXItems;
+  if (base >= m.scalars) return;
+  const double* src = m.slab + (a.n & 1) * m.scalars;
+#pragma unroll
+  for (int it = 0; it < kXItems; ++it) {
+    const long long q = base + it * kXThreads + threadIdx.x;
+    if (q < m.scalars) {
+      int v, i, j, k;
+      msg_locate(m, q, v, i, j, k);
+      double x = __ldcg(src + q);
+      if (a.corrupt && blockIdx.y == 0 && q == 0) x += 1e-3;  // exchange_finish's hook
+      a.state[v * a.g.fstride + a.g.idx(i, j, k)] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scalar exchange: every rank pushes (CFL maxima, centre pressure, error code)
+// into slot[rank][n&1] of every rank's arena, then folds all np slots.
+struct Slot {
+  unsigned long long d[3];
+  double pc;
+  unsigned long long err;
+  unsigned long long stamp;
+  unsigned long long pad[2];
+};
+static_assert(sizeof(Slot) == 64, "slot size");
+
+struct SyncArgs {
+  Acc* acc_cur;
+  Acc* acc_next;
+  IterScalars* sc_next;
+  Slot* my_slots;              // this rank's arena slots [np][2]
+  Slot* const* peer_slots;     // device array: rank r's slot base
+  int np, rank, owner;
+  long long n;
+  double dx, dy, dz, cfl;
+  cav_fluid_params fl;
+  int rescale;
+  unsigned long long* err_sticky;
+  unsigned long long timeout_ns;
+  unsigned long long* timeout_flag;
+};
+
+constexpr int kSyncThreads = 128;
+
+__global__ void __launch_bounds__(kSyncThreads) k_scalar_sync(const SyncArgs a) {
+  __shared__ unsigned long long sd[3][kSyncThreads];
+  __shared__ unsigned long long se[kSyncThreads];
+  __shared__ double spc;
+  const int tid = threadIdx.x;
+  const int par = static_cast<int>(a.n & 1);
+  const Acc mine = *a.acc_cur;
+  if (tid == 0) spc = 0.0;
+  for (int r = tid; r < a.np; r += kSyncThreads) {
+    Slot* s = a.peer_slots[r] + (a.rank * 2 + par);
+    s->d[0] = mine.dmax[0];
+    s->d[1] = mine.dmax[1];
+    s->d[2] = mine.dmax[2];
+    s->pc = mine.pc_local;
+    s->err = mine.err;
+    __threadfence_system();
+    st_release_sys(&s->stamp, static_cast<unsigned long long>(a.n));
+  }
+  unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
+  __syncthreads();
+  for (int r = tid; r < a.np; r += kSyncThreads) {
+    const Slot* s = a.my_slots + (r * 2 + par);
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(&s->stamp) < static_cast<unsigned long long>(a.n)) {
+      if (globaltimer_ns() - t0 > a.timeout_ns) {
+        atomicMin(a.timeout_flag, err_code(a.n, r, 15));
+        break;
+      }
+      __nanosleep(32);
+    }
+    d0 = max(d0, __ldcg(&s->d[0]));
+    d1 = max(d1, __ldcg(&s->d[1]));
+    d2 = max(d2, __ldcg(&s->d[2]));
+    e = min(e, __ldcg(&s->err));
+    if (r == a.owner) spc = __ldcg(&s->pc);
+  }
+  sd[0][tid] = d0;
+  sd[1][tid] = d1;
+  sd[2][tid] = d2;
+  se[tid] = e;
+  __syncthreads();
+  if (tid == 0) {
+    for (int t = 1; t < kSyncThreads; ++t) {
+      d0 = max(d0, sd[0][t]);
+      d1 = max(d1, sd[1][t]);
+      d2 = max(d2, sd[2][t]);
+      e = min(e, se[t]);
+    }
+    const unsigned long long dm[3] = {d0, d1, d2};
+    a.sc_next->dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, a.fl, a.cfl);
+    a.sc_next->pc = (a.rescale && a.n >= 1) ? spc : 0.0;
+    if (e < *a.err_sticky) *a.err_sticky = e;
+    Acc z{};
+    z.err = ~0ull;
+    *a.acc_next = z;
+  }
+}
+
+// Whole-storage export in the reference Field3 layout: interior from `cur`
+// with the pending shift, every ghost from `prev` (the last input state, whose
+// ghosts are exactly what the reference's storage holds after the loop).
+__global__ void k_export(const double* cur, const double* prev, Geo g, double pc, double* out) {
+  const long long X = g.nx + 4, Y = g.ny + 4, Z = g.nz + 4, S = X * Y * Z;
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= 5 * S) return;
+  const int v = static_cast<int>(q / S);
+  const long long e = q % S;
+  const int i = static_cast<int>(e % X), j = static_cast<int>((e / X) % Y), k = static_cast<int>(e / (X * Y));
+  const long long c = v * g.fstride + g.idx(i, j, k);
+  double x;
+  if (g.interior(i, j, k)) {
+    x = cur[c];
+    if (v == 0) x = x - pc;
+  } else {
+    x = prev[c];
+  }
+  out[q] = x;
+}
+
+__global__ void k_fill_ic(double* s0, double* s1, Geo g, double t_inf) {
+  const long long X = g.nx + 4, Y = g.ny + 4, Z = g.nz + 4, S = X * Y * Z;
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= 5 * S) return;
+  const int v = static_cast<int>(q / S);
+  const long long e = q % S;
+  const int i = static_cast<int>(e % X), j = static_cast<int>((e / X) % Y), k = static_cast<int>(e / (X * Y));
+  const long long c = v * g.fstride + g.idx(i, j, k);
+  const double x = v == 4 ? t_inf : 0.0;  // initialize_fields (src/solver.cpp:292-298)
+  s0[c] = x;
+  s1[c] = x;
+}
+
+// ---------------------------------------------------------------------------
+// Host side of a block.
+namespace {
+
+constexpr size_t kFlagBytes = 64 * sizeof(unsigned long long);
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct ArenaLayout {
+  size_t slots = 0;                 // offset of Slot[np][2]
+  std::vector<size_t> slab;         // per plan entry (receiver side)
+  size_t bytes = 0;
+};
+
+ArenaLayout arena_layout(const std::vector<cav_plan_entry>& plan, int np) {
+  ArenaLayout L;
+  L.slots = kFlagBytes;
+  size_t off = align_up(L.slots + static_cast<size_t>(np) * 2 * sizeof(Slot), 256);
+  for (const auto& e : plan) {
+    L.slab.push_back(off);
+    off = align_up(off + 2 * static_cast<size_t>(e.scalars) * sizeof(double), 256);
+  }
+  L.bytes = off;
+  return L;
+}
+
+int find_entry(const std::vector<cav_plan_entry>& plan, int face, const cav_plan_entry& like) {
+  for (size_t n = 0; n < plan.size(); ++n)
+    if (plan[n].face == face && plan[n].nvars == like.nvars && plan[n].var[0] == like.var[0])
+      return static_cast<int>(n);
+  throw std::logic_error("exchange: no matching receive entry on the neighbour");
+}
+
+cudaEvent_t make_event() {
+  cudaEvent_t e;
+  CAV_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+}  // namespace
+
+struct Block {
+  cav_block_desc d{};
+  std::array<int, 3> gn{}, dims{}, n{};
+  std::vector<host::Extent> ext;
+  std::array<int, 6> rank_at{};
+  int walls[6]{};
+  int owner = 0;
+  int cx = -1, cy = -1, cz = -1;
+  double dx = 0, dy = 0, dz = 0;
+  cav_stencil_params sp{};
+  Geo g{};
+  double* state[2]{};
+  int cur = 0;
+  std::vector<cav_plan_entry> plan;
+  ArenaLayout lay;
+  unsigned char* arena = nullptr;
+  std::vector<unsigned char*> peer_arena;
+  std::vector<bool> peer_ipc;
+  cav_box internal{};
+  std::vector<cav_box> shells;
+  // device bookkeeping
+  Acc* acc = nullptr;            // [2]
+  IterScalars* sc = nullptr;     // [2]
+  unsigned long long* err = nullptr;      // sticky min error code
+  unsigned long long* tflag = nullptr;    // timeout code
+  unsigned* counters = nullptr;
+  MsgDesc* d_pack = nullptr;
+  MsgDesc* d_unpack = nullptr;
+  Slot** d_peer_slots = nullptr;
+  unsigned long long* digits = nullptr;
+  long long digits_cap = 0;
+  bool ready = false;
+  long long next_n = 1;
+  bool primed = false;
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_a = nullptr, ev_b = nullptr;
+  std::vector<cudaEvent_t> kev;  // bench: per-step kernel timing
+  int kind_ty = 8;
+  int kchunk = 0;
+
+  explicit Block(const cav_block_desc& desc);
+  ~Block();
+  double* field(int s, int v) const { return state[s] + v * g.fstride; }
+  void ensure_ready();
+  void prologue();
+  void iteration(long long it, bool check, unsigned long long* dig, bool timed_kernel);
+  void launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig);
+  void launch_shells(long long it, bool check, unsigned long long* dig);
+  void update_ledger(cav_ledger& l) const;
+};
+
+Block::Block(const cav_block_desc& desc) : d(desc) {
+  host::validate_params(d.fluid);
+  gn = {d.gnx, d.gny, d.gnz};
+  dims = {d.dims[0], d.dims[1], d.dims[2]};
+  if (dims[0] * dims[1] * dims[2] != d.np) throw std::invalid_argument("block: dims do not multiply to np");
+  if (d.rank < 0 || d.rank >= d.np) throw std::invalid_argument("rank out of range");
+  const auto h = host::cavity_spacing(gn[0], gn[1], gn[2], d.fluid.length, d.fluid.length, d.fluid.length);
+  dx = h[0];
+  dy = h[1];
+  dz = h[2];
+  ext = host::partition(gn, dims);
+  const host::Extent& e = ext[d.rank];
+  n = {e.size(0), e.size(1), e.size(2)};
+  host::validate_grid(n[0], n[1], n[2], dx, dy, dz);
+  rank_at = host::neighbors(dims, d.rank);
+  for (int f = 0; f < 6; ++f) walls[f] = rank_at[f] == CAV_WALL;
+  const auto c = host::center_node(gn);
+  owner = host::owner_of(ext, c);
+  if (owner == d.rank) {
+    cx = c[0] - e.lo[0] + 2;
+    cy = c[1] - e.lo[1] + 2;
+    cz = c[2] - e.lo[2] + 2;
+  }
+  sp = host::stencil_params(dx, dy, dz, d.fluid);
+  plan = host::build_plan(n, rank_at, d.strategy);
+  host::overlap_regions(n, rank_at, &internal, shells);
+  lay = arena_layout(plan, d.np);
+
+  CAV_CUDA(cudaSetDevice(d.device));
+  // padded layout: interior rows start 128-byte aligned (off 14 -> i=2 at 16)
+  g.nx = n[0];
+  g.ny = n[1];
+  g.nz = n[2];
+  g.off = 14;
+  g.pitch = static_cast<int>(align_up(static_cast<size_t>(g.off + n[0] + 4), 16));
+  g.ypitch = n[1] + 4;
+  g.fstride = static_cast<long long>(align_up(static_cast<size_t>(g.pitch) * g.ypitch * (n[2] + 4), 32));
+  for (int s = 0; s < 2; ++s) {
+    CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
+    CAV_CUDA(cudaMemset(state[s], 0, 5 * g.fstride * sizeof(double)));
+  }
+  CAV_CUDA(cudaMalloc(&arena, lay.bytes));
+  CAV_CUDA(cudaMemset(arena, 0, lay.bytes));
+  CAV_CUDA(cudaMalloc(&acc, 2 * sizeof(Acc)));
+  CAV_CUDA(cudaMalloc(&sc, 2 * sizeof(IterScalars)));
+  CAV_CUDA(cudaMalloc(&err, 2 * sizeof(unsigned long long)));
+  tflag = err + 1;
+  CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
+  CAV_CUDA(cudaMemset(counters, 0, 64 * sizeof(unsigned)));
+  CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
+  if (!plan.empty()) {
+    CAV_CUDA(cudaMalloc(&d_pack, plan.size() * sizeof(MsgDesc)));
+    CAV_CUDA(cudaMalloc(&d_unpack, plan.size() * sizeof(MsgDesc)));
+  }
+  int lo, hi;
+  CAV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CAV_CUDA(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, lo));
+  CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, hi));  // comm: high priority
+  CAV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  CAV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  ev_a = make_event();
+  ev_b = make_event();
+  peer_arena.assign(d.np, nullptr);
+  peer_ipc.assign(d.np, false);
+  peer_arena[d.rank] = arena;
+}
+
+Block::~Block() {
+  cudaSetDevice(d.device);
+  if (s0) cudaStreamSynchronize(s0);
+  if (s1) cudaStreamSynchronize(s1);
+  for (int r = 0; r < d.np; ++r)
+    if (peer_ipc[r] && peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
+  for (auto e : kev) cudaEventDestroy(e);
+  cudaFree(state[0]);
+  cudaFree(state[1]);
+  cudaFree(arena);
+  cudaFree(acc);
+  cudaFree(sc);
+  cudaFree(err);
+  cudaFree(counters);
+  cudaFree(d_peer_slots);
+  cudaFree(d_pack);
+  cudaFree(d_unpack);
+  cudaFree(digits);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (s0) cudaStreamDestroy(s0);
+  if (s1) cudaStreamDestroy(s1);
+}
+
+void Block::ensure_ready() {
+  if (ready) return;
+  for (int r = 0; r < d.np; ++r)
+    if (!peer_arena[r])
+      throw std::logic_error("block: rank " + std::to_string(r) + " not connected (cav_block_connect)");
+  std::vector<Slot*> ps(d.np);
+  for (int r = 0; r < d.np; ++r) ps[r] = reinterpret_cast<Slot*>(peer_arena[r] + lay.slots);
+  CAV_CUDA(cudaMemcpy(d_peer_slots, ps.data(), d.np * sizeof(Slot*), cudaMemcpyHostToDevice));
+  std::vector<MsgDesc> pk(plan.size()), up(plan.size());
+  for (size_t m = 0; m < plan.size(); ++m) {
+    const cav_plan_entry& e = plan[m];
+    MsgDesc a{};
+    a.face = e.face;
+    a.nvars = e.nvars;
+    a.scalars = e.scalars;
+    a.peer = e.neighbor;
+    long long off = 0;
+    for (int v = 0; v < e.nvars; ++v) a.var[v] = e.var[v];
+    MsgDesc b = a;
+    for (int v = 0; v < e.nvars; ++v) {
+      a.voff[v] = off;
+      b.voff[v] = off;
+      a.box[v] = host::face_box(n, e.face, e.depth[v], false);
+      b.box[v] = host::face_box(n, e.face, e.depth[v], true);
+      off += host::box_volume(a.box[v]);
+    }
+    a.voff[e.nvars] = b.voff[e.nvars] = off;
+    // the neighbour receives on the opposite face into its own plan's entry
+    const host::Extent& ne = ext[e.neighbor];
+    const std::array<int, 3> nn{ne.size(0), ne.size(1), ne.size(2)};
+    const auto nplan = host::build_plan(nn, host::neighbors(dims, e.neighbor), d.strategy);
+    const ArenaLayout nl = arena_layout(nplan, d.np);
+    const int ri = find_entry(nplan, e.face ^ 1, e);
+    a.slab = reinterpret_cast<double*>(peer_arena[e.neighbor] + nl.slab[ri]);
+    a.flag = reinterpret_cast<unsigned long long*>(peer_arena[e.neighbor]) + ri;
+    a.counter = counters + m;
+    b.slab = reinterpret_cast<double*>(arena + lay.slab[m]);
+    b.flag = reinterpret_cast<unsigned long long*>(arena) + m;
+    pk[m] = a;
+    up[m] = b;
+  }
+  if (!plan.empty()) {
+    CAV_CUDA(cudaMemcpy(d_pack, pk.data(), pk.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice));
+    CAV_CUDA(cudaMemcpy(d_unpack, up.data(), up.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice));
+  }
+  // tile shape: 32 x 8 threads, k split so the grid fills ~2 waves of 148 SMs
+  const long long tiles = ((n[0] + 31) / 32) * static_cast<long long>((n[1] + 7) / 8);
+  const long long want = 148 * 4;
+  int chunks = static_cast<int>(std::max<long long>(1, (want + tiles - 1) / tiles));
+  chunks = std::min(chunks, std::max(1, n[2] / 16));
+  kchunk = (n[2] + chunks - 1) / chunks;
+  ready = true;
+}
+
+void Block::prologue() {
+  Acc z[2] = {};
+  z[0].err = z[1].err = ~0ull;
+  CAV_CUDA(cudaMemcpyAsync(acc, z, sizeof z, cudaMemcpyHostToDevice, s0));
+  CAV_CUDA(cudaMemsetAsync(sc, 0, 2 * sizeof(IterScalars), s0));
+  const unsigned long long e0[2] = {~0ull, ~0ull};
+  CAV_CUDA(cudaMemcpyAsync(err, e0, sizeof e0, cudaMemcpyHostToDevice, s0));
+  const cav_field_ptrs f{field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
+  const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
+  ops::launch_dt_scan(f, g, ib, sp.u_ref, acc, 1, d.rank, s0);  // dt_1 from the initial state
+  SyncArgs a{};
+  a.acc_cur = acc;
+  a.acc_next = acc + 1;
+  a.sc_next = sc + 1;
+  a.my_slots = reinterpret_cast<Slot*>(arena + lay.slots);
+  a.peer_slots = d_peer_slots;
+  a.np = d.np;
+  a.rank = d.rank;
+  a.owner = owner;
+  a.n = 0;
+  a.dx = dx;
+  a.dy = dy;
+  a.dz = dz;
+  a.cfl = d.cfl;
+  a.fl = d.fluid;
+  a.rescale = d.rescale;
+  a.err_sticky = err;
+  a.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
+  a.timeout_flag = tflag;
+  k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
+  CAV_CUDA(cudaGetLastError());
+  primed = true;
+}
+
+void Block::launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig) {
+  const long long vol = host::box_volume(box);
+  if (vol == 0) return;
+  StepArgs a{};
+  a.in = state[cur];
+  a.out = state[cur ^ 1];
+  a.g = g;
+  a.sp = sp;
+  a.box = box;
+  a.sc = sc + (it & 1);
+  a.acc = acc + (it & 1);
+  a.digits = dig;
+  a.cx = cx;
+  a.cy = cy;
+  a.cz = cz;
+  a.n = it;
+  a.rank = d.rank;
+  const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
+  a.kchunk = std::min(kchunk, bd);
+  const dim3 grid((bw + 31) / 32, (bh + 7) / 8, (bd + a.kchunk - 1) / a.kchunk);
+  const dim3 block(32, 8);
+  if (check) k_step_tiled<8, true><<<grid, block, 0, s0>>>(a);
+  else k_step_tiled<8, false><<<grid, block, 0, s0>>>(a);
+  CAV_CUDA(cudaGetLastError());
+}
+
+void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
+  if (shells.empty()) return;
+  ShellArgs a{};
+  a.s.in = state[cur];
+  a.s.out = state[cur ^ 1];
+  a.s.g = g;
+  a.s.sp = sp;
+  a.s.sc = sc + (it & 1);
+  a.s.acc = acc + (it & 1);
+  a.s.digits = dig;
+  a.s.cx = cx;
+  a.s.cy = cy;
+  a.s.cz = cz;
+  a.s.n = it;
+  a.s.rank = d.rank;
+  a.nbox = static_cast<int>(shells.size());
+  a.start[0] = 0;
+  for (int b = 0; b < a.nbox; ++b) {
+    a.box[b] = shells[b];
+    a.start[b + 1] = a.start[b] + host::box_volume(shells[b]);
+  }
+  const int nb = static_cast<int>((a.start[a.nbox] + kShellThreads - 1) / kShellThreads);
+  if (check) k_step_shells<true><<<nb, kShellThreads, 0, s0>>>(a);
+  else k_step_shells<false><<<nb, kShellThreads, 0, s0>>>(a);
+  CAV_CUDA(cudaGetLastError());
+}
+
+void Block::iteration(long long it, bool check, unsigned long long* dig, bool timed_kernel) {
+  const IterScalars* sc_n = sc + (it & 1);
+  double* f[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
+  ops::launch_bc(f, g, walls, d.fluid, sc_n, s0);
+  XArgs x{};
+  x.state = state[cur];
+  x.g = g;
+  x.n = it;
+  x.sc = sc_n;
+  x.corrupt = d.corrupt_exchange;
+  x.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
+  x.timeout_flag = tflag;
+  x.rank = d.rank;
+  long long maxs = 0;
+  for (const auto& e : plan) maxs = std::max(maxs, e.scalars);
+  const dim3 xgrid(static_cast<unsigned>((maxs + kXThreads * kXItems - 1) / (kXThreads * kXItems)),
+                   static_cast<unsigned>(plan.size()));
+  const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
+  cudaEvent_t* kt = nullptr;
+  if (timed_kernel) {
+    kev.push_back(make_event());
+    kev.push_back(make_event());
+    kt = &kev[kev.size() - 2];
+  }
+  if (plan.empty()) {
+    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
+    launch_step(ib, it, check, dig);
+    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+  } else if (!d.overlap) {
+    x.msg = d_pack;
+    k_pack<<<xgrid, kXThreads, 0, s0>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    x.msg = d_unpack;
+    k_wait_flags<<<1, 32, 0, s0>>>(x, static_cast<int>(plan.size()));
+    CAV_CUDA(cudaGetLastError());
+    k_unpack<<<xgrid, kXThreads, 0, s0>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
+    launch_step(ib, it, check, dig);
+    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+  } else {
+    // overlap (src/runner.cpp:189-194): exchange on the high-priority comm
+    // stream while the internal box computes; shells after the join
+    CAV_CUDA(cudaEventRecord(ev_fork, s0));
+    CAV_CUDA(cudaStreamWaitEvent(s1, ev_fork, 0));
+    x.msg = d_pack;
+    k_pack<<<xgrid, kXThreads, 0, s1>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    x.msg = d_unpack;
+    k_wait_flags<<<1, 32, 0, s1>>>(x, static_cast<int>(plan.size()));
+    CAV_CUDA(cudaGetLastError());
+    k_unpack<<<xgrid, kXThreads, 0, s1>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    CAV_CUDA(cudaEventRecord(ev_join, s1));
+    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
+    launch_step(internal, it, check, dig);
+    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+    CAV_CUDA(cudaStreamWaitEvent(s0, ev_join, 0));
+    launch_shells(it, check, dig);
+  }
+  SyncArgs a{};
+  a.acc_cur = acc + (it & 1);
+  a.acc_next = acc + ((it + 1) & 1);
+  a.sc_next = sc + ((it + 1) & 1);
+  a.my_slots = reinterpret_cast<Slot*>(arena + lay.slots);
+  a.peer_slots = d_peer_slots;
+  a.np = d.np;
+  a.rank = d.rank;
+  a.owner = owner;
+  a.n = it;
+  a.dx = dx;
+  a.dy = dy;
+  a.dz = dz;
+  a.cfl = d.cfl;
+  a.fl = d.fluid;
+  a.rescale = d.rescale;
+  a.err_sticky = err;
+  a.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
+  a.timeout_flag = tflag;
+  k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
+  CAV_CUDA(cudaGetLastError());
+  cur ^= 1;
+}
+
+void Block::update_ledger(cav_ledger& l) const {
+  // exchange_begin/record_send (src/exchange.cpp:30-42, :115-145): one
+  // begin_exchange per iteration, one record per plan entry
+  ++l.exchanges;
+  for (auto& b : l.last_face_bytes) b = 0;
+  for (const auto& e : plan) {
+    const uint64_t bytes = static_cast<uint64_t>(e.scalars) * sizeof(double);
+    l.face_bytes[e.face] += bytes;
+    l.last_face_bytes[e.face] += bytes;
+    l.face_messages[e.face] += 1;
+    l.bytes_sent += bytes;
+    l.messages_sent += 1;
+  }
+}
+
+namespace {
+const char* kVar[5] = {"p", "u", "v", "w", "T"};
+
+std::string error_message(unsigned long long code) {
+  const long long it = static_cast<long long>(code >> 24);
+  const int kind = static_cast<int>(code & 15);
+  if (kind == 0) return "iteration " + std::to_string(it) + ": repro_sum: non-finite term";
+  return "iteration " + std::to_string(it) + ": compute_dt: non-finite value in field " + kVar[kind - 1];
+}
+}  // namespace
+
+}  // namespace cav
+
+using namespace cav;
+
+struct cav_block {
+  std::unique_ptr<Block> b;
+};
+
+extern "C" {
+
+const char* cav_version(void) {
+#ifdef CAV_FMAD
+  return "cavity_b200 sm_100a fmad=true (tolerance build)";
+#else
+  return "cavity_b200 sm_100a fmad=false (bitwise build)";
+#endif
+}
+
+int cav_block_create(const cav_block_desc* desc, cav_block** out) {
+  return guarded([&] {
+    auto h = std::make_unique<cav_block>();
+    h->b = std::make_unique<Block>(*desc);
+    *out = h.release();
+  });
+}
+
+int cav_block_destroy(cav_block* b) {
+  return guarded([&] { delete b; });
+}
+
+int cav_block_arena(cav_block* b, void** ptr, size_t* bytes) {
+  return guarded([&] {
+    *ptr = b->b->arena;
+    *bytes = b->b->lay.bytes;
+  });
+}
+
+int cav_block_arena_ipc(cav_block* b, unsigned char handle[64]) {
+  return guarded([&] {
+    CAV_CUDA(cudaSetDevice(b->b->d.device));
+    cudaIpcMemHandle_t h;
+    CAV_CUDA(cudaIpcGetMemHandle(&h, b->b->arena));
+    static_assert(sizeof h == 64, "ipc handle size");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+int cav_block_connect(cav_block* bh, int r, void* ptr, const unsigned char* ipc) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    if (r < 0 || r >= b.d.np) throw std::invalid_argument("connect: rank out of range");
+    if ((ptr == nullptr) == (ipc == nullptr)) throw std::invalid_argument("connect: pass exactly one of ptr/ipc");
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    if (r == b.d.rank) return;  // own arena is always connected
+    if (ptr) {
+      cudaPointerAttributes at{};
+      CAV_CUDA(cudaPointerGetAttributes(&at, ptr));
+      if (at.device != b.d.device) {
+        int ok = 0;
+        CAV_CUDA(cudaDeviceCanAccessPeer(&ok, b.d.device, at.device));
+        if (!ok) throw std::runtime_error("connect: no peer access from device " + std::to_string(b.d.device) +
+                                          " to " + std::to_string(at.device));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CAV_CUDA(e);
+        cudaGetLastError();
+      }
+      b.peer_arena[r] = static_cast<unsigned char*>(ptr);
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, ipc, 64);
+      void* p = nullptr;
+      CAV_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      b.peer_arena[r] = static_cast<unsigned char*>(p);
+      b.peer_ipc[r] = true;
+    }
+    b.ready = false;
+  });
+}
+
+int cav_block_upload(cav_block* bh, const double* host5) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    const size_t X = b.n[0] + 4, Y = b.n[1] + 4, Z = b.n[2] + 4;
+    for (int s = 0; s < 2; ++s)
+      for (int v = 0; v < 5; ++v)
+        CAV_CUDA(cudaMemcpy2D(b.field(s, v) + b.g.off, b.g.pitch * sizeof(double), host5 + v * X * Y * Z,
+                              X * sizeof(double), X * sizeof(double), Y * Z, cudaMemcpyHostToDevice));
+    b.cur = 0;
+    b.next_n = 1;
+    b.primed = false;
+  });
+}
+
+int cav_block_initialize(cav_block* bh) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    const long long S = static_cast<long long>(b.n[0] + 4) * (b.n[1] + 4) * (b.n[2] + 4);
+    k_fill_ic<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.state[0], b.state[1], b.g,
+                                                                            b.d.fluid.t_inf);
+    CAV_CUDA(cudaGetLastError());
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
+    b.cur = 0;
+    b.next_n = 1;
+    b.primed = false;
+  });
+}
+
+int cav_block_download(cav_block* bh, double* host5) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    const long long S = static_cast<long long>(b.n[0] + 4) * (b.n[1] + 4) * (b.n[2] + 4);
+    double pc = 0.0;
+    if (b.primed) {
+      IterScalars s{};
+      CAV_CUDA(cudaMemcpyAsync(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost, b.s0));
+      CAV_CUDA(cudaStreamSynchronize(b.s0));
+      if (b.next_n > 1) pc = s.pc;
+    }
+    double* tmp = nullptr;
+    CAV_CUDA(cudaMallocAsync(&tmp, 5 * S * sizeof(double), b.s0));
+    k_export<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.state[b.cur], b.state[b.cur ^ 1],
+                                                                           b.g, pc, tmp);
+    CAV_CUDA(cudaGetLastError());
+    CAV_CUDA(cudaMemcpyAsync(host5, tmp, 5 * S * sizeof(double), cudaMemcpyDeviceToHost, b.s0));
+    CAV_CUDA(cudaFreeAsync(tmp, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
+  });
+}
+
+int cav_block_run(cav_block* bh, cav_run_io* io) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    if (io->first_it != b.next_n)
+      throw std::logic_error("block_run: iterations must continue at " + std::to_string(b.next_n));
+    if (!(b.d.cfl > 0.0) || !std::isfinite(b.d.cfl))
+      throw std::runtime_error("iteration " + std::to_string(io->first_it) + ": compute_dt: cfl must be positive, got " +
+                               host::fmt_double_f(b.d.cfl));
+    b.ensure_ready();
+    const long long first = io->first_it, last = io->first_it + io->n_its - 1;
+    const int cadence = std::max(1, io->check_every);
+    auto is_check = [&](long long it) { return io->want_norms && (it == 1 || it % cadence == 0); };
+    long long nchk = 0;
+    for (long long it = first; it <= last; ++it) nchk += is_check(it);
+    if (nchk > b.digits_cap) {
+      cudaFree(b.digits);
+      CAV_CUDA(cudaMalloc(&b.digits, nchk * 5 * kDigits * sizeof(unsigned long long)));
+      b.digits_cap = nchk;
+    }
+    if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
+    if (!b.primed) b.prologue();
+    bool started = false;
+    if (first != 1) {
+      CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
+      started = true;
+    }
+    long long ci = 0;
+    for (long long it = first; it <= last; ++it) {
+      const bool chk = is_check(it);
+      unsigned long long* dig = chk ? b.digits + ci * 5 * kDigits : nullptr;
+      if (chk && io->check_iters) io->check_iters[ci] = it;
+      ci += chk;
+      b.iteration(it, chk, dig, false);
+      b.update_ledger(io->ledger);
+      if (it == 1) {  // iteration 1 is warm-up (src/runner.cpp:186)
+        CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
+        started = true;
+      }
+    }
+    CAV_CUDA(cudaEventRecord(b.ev_b, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
+    float ms = 0.f;
+    if (started && io->n_its > 0) CAV_CUDA(cudaEventElapsedTime(&ms, b.ev_a, b.ev_b));
+    io->seconds = ms * 1e-3;
+    b.next_n = last + 1;
+    io->n_checks = nchk;
+    if (nchk && io->norm_digits)
+      CAV_CUDA(cudaMemcpy(io->norm_digits, b.digits, nchk * 5 * kDigits * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost));
+    unsigned long long codes[2];
+    CAV_CUDA(cudaMemcpy(codes, b.err, sizeof codes, cudaMemcpyDeviceToHost));
+    io->err_iteration = 0;
+    io->err_kind = 0;
+    if (codes[1] != ~0ull) {
+      const int kind = static_cast<int>(codes[1] & 15);
+      const int who = static_cast<int>((codes[1] >> 4) & 0xFFFFF);
+      throw Timeout(kind == 15 ? "transport timeout: rank " + std::to_string(b.d.rank) +
+                                     " waiting for scalars from rank " + std::to_string(who)
+                               : "transport timeout: rank " + std::to_string(b.d.rank) + " waiting on face " +
+                                     std::to_string(kind - 8));
+    }
+    if (codes[0] != ~0ull && static_cast<long long>(codes[0] >> 24) <= last) {
+      io->err_iteration = static_cast<long long>(codes[0] >> 24);
+      io->err_kind = static_cast<int>(codes[0] & 15);
+      throw std::runtime_error(error_message(codes[0]));
+    }
+  });
+}
+
+int cav_block_launches_per_iteration(cav_block* bh, int check) {
+  Block& b = *bh->b;
+  (void)check;
+  int walls = 0;
+  for (int f = 0; f < 6; ++f) walls += b.walls[f];
+  int n = (walls ? 1 : 0) + 1 + 1;  // bc, step, sync
+  if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);
+  return n;
+}
+
+int cav_block_scalars(cav_block* bh, double* dt, double* pc) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    IterScalars s{};
+    CAV_CUDA(cudaMemcpy(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost));
+    *dt = s.dt;
+    *pc = s.pc;
+  });
+}
+
+int cav_block_bench(cav_block* bh, long long n_its, double* total_ms, double* step_ms) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    b.ensure_ready();
+    if (!b.primed) b.prologue();
+    for (auto e : b.kev) cudaEventDestroy(e);
+    b.kev.clear();
+    CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
+    for (long long k = 0; k < n_its; ++k) b.iteration(b.next_n + k, false, nullptr, true);
+    CAV_CUDA(cudaEventRecord(b.ev_b, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
+    b.next_n += n_its;
+    float ms = 0.f;
+    CAV_CUDA(cudaEventElapsedTime(&ms, b.ev_a, b.ev_b));
+    *total_ms = ms;
+    double ks = 0.0;
+    for (size_t q = 0; q + 1 < b.kev.size(); q += 2) {
+      float t = 0.f;
+      CAV_CUDA(cudaEventElapsedTime(&t, b.kev[q], b.kev[q + 1]));
+      ks += t;
+    }
+    *step_ms = n_its ? ks / static_cast<double>(n_its) : 0.0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// device.cuh — device building blocks shared by the op-level parity kernels
+// (ops.cu) and the block-level fused pipeline (block.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cell.cuh"
+
+namespace cav {
+
+// Per-iteration scalars every kernel of iteration n reads: the step dt_n and
+// the pending centre-pressure shift pc_{n-1} (0 when rescale is off or n==1).
+struct IterScalars {
+  double dt;
+  double pc;
+};
+
+// Per-iteration accumulators written by the fused step (and the prologue scan).
+struct Acc {
+  unsigned long long dmax[3];  // bit patterns of max(|u|+beta), ... (all >= u_ref > 0)
+  unsigned long long err;      // min error code, ~0 = none
+  double pc_local;             // p' at the centre node, on its owner
+  unsigned long long pad[3];
+};
+
+// Error code ordering = the reference's reporting order: earliest iteration,
+// then lowest rank (run_case prefers the lowest non-echo rank,
+// src/runner.cpp:294-309), then kind (norms are evaluated before compute_dt,
+// src/runner.cpp:200-223): kind 0 = "repro_sum: non-finite term",
+// 1..5 = "compute_dt: non-finite value in field p,u,v,w,T".
+__host__ __device__ __forceinline__ unsigned long long err_code(long long it, int rank, int kind) {
+  return (static_cast<unsigned long long>(it) << 24) | (static_cast<unsigned long long>(rank) << 4) |
+         static_cast<unsigned long long>(kind);
+}
+
+__device__ __forceinline__ double dmax_d(double a, double b) { return a < b ? b : a; }
+
+// Loads one cell's star from global memory (layout g). Pressure values of
+// interior cells get the pending rescale shift fl(p - pc); ghost values are
+// already final. Subtracting +0.0 is the exact identity, so shift==0.0 means
+// "no rescale pending".
+__device__ __forceinline__ Star load_star(const double* __restrict__ P, const double* __restrict__ U,
+                                          const double* __restrict__ V, const double* __restrict__ W,
+                                          const double* __restrict__ T, const Geo& g, int i, int j,
+                                          int k, double pc) {
+  const long long c = g.idx(i, j, k);
+  const long long sj = g.pitch, sk = static_cast<long long>(g.pitch) * g.ypitch;
+  auto ps = [&](long long off, int ii, int jj, int kk) {
+    const double x = P[c + off];
+    return x - (g.interior(ii, jj, kk) ? pc : 0.0);
+  };
+  Star s;
+  s.p = ps(0, i, j, k);
+  s.pxm = ps(-1, i - 1, j, k);
+  s.pxp = ps(1, i + 1, j, k);
+  s.pxm2 = ps(-2, i - 2, j, k);
+  s.pxp2 = ps(2, i + 2, j, k);
+  s.pym = ps(-sj, i, j - 1, k);
+  s.pyp = ps(sj, i, j + 1, k);
+  s.pym2 = ps(-2 * sj, i, j - 2, k);
+  s.pyp2 = ps(2 * sj, i, j + 2, k);
+  s.pzm = ps(-sk, i, j, k - 1);
+  s.pzp = ps(sk, i, j, k + 1);
+  s.pzm2 = ps(-2 * sk, i, j, k - 2);
+  s.pzp2 = ps(2 * sk, i, j, k + 2);
+#define CAV_Q7(F, A)           \
+  s.F = A[c];                  \
+  s.F##xm = A[c - 1];          \
+  s.F##xp = A[c + 1];          \
+  s.F##ym = A[c - sj];         \
+  s.F##yp = A[c + sj];         \
+  s.F##zm = A[c - sk];         \
+  s.F##zp = A[c + sk];
+  CAV_Q7(u, U)
+  CAV_Q7(v, V)
+  CAV_Q7(w, W)
+  CAV_Q7(t, T)
+#undef CAV_Q7
+  return s;
+}
+
+// Block-wide max of three doubles and OR of a mask; thread 0 gets the result.
+template <int NT>
+__device__ __forceinline__ void block_reduce_max3_or(double& a, double& b, double& c, unsigned& m) {
+  __shared__ double sred[3][NT / 32];
+  __shared__ unsigned smask[NT / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a = dmax_d(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = dmax_d(b, __shfl_xor_sync(0xffffffffu, b, o));
+    c = dmax_d(c, __shfl_xor_sync(0xffffffffu, c, o));
+  }
+  m = __reduce_or_sync(0xffffffffu, m);
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+    sred[0][warp] = a;
+    sred[1][warp] = b;
+    sred[2][warp] = c;
+    smask[warp] = m;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < NT / 32; ++w) {
+      a = dmax_d(a, sred[0][w]);
+      b = dmax_d(b, sred[1][w]);
+      c = dmax_d(c, sred[2][w]);
+      m |= smask[w];
+    }
+  }
+}
+
+// Publishes a block's CFL maxima / non-finite mask into an accumulator.
+// Non-negative doubles order like their bit patterns, so an unsigned atomicMax
+// on the bits is an exact max.
+__device__ __forceinline__ void acc_publish(Acc* acc, double a, double b, double c, unsigned mask,
+                                            long long it_for_dt, int rank) {
+  atomicMax(&acc->dmax[0], static_cast<unsigned long long>(__double_as_longlong(a)));
+  atomicMax(&acc->dmax[1], static_cast<unsigned long long>(__double_as_longlong(b)));
+  atomicMax(&acc->dmax[2], static_cast<unsigned long long>(__double_as_longlong(c)));
+  if (mask) atomicMin(&acc->err, err_code(it_for_dt, rank, 1 + __ffs(mask) - 1));
+}
+
+__device__ __forceinline__ void add_term_digits(unsigned long long* dig, double x) {
+  if (x == 0.0) return;
+  const TermPieces tp = term_pieces(x);
+  atomicAdd(&dig[tp.d], static_cast<unsigned long long>(tp.a));
+  atomicAdd(&dig[tp.d + 1], static_cast<unsigned long long>(tp.b));
+  if (tp.c) atomicAdd(&dig[tp.d + 2], static_cast<unsigned long long>(tp.c));
+}
+
+// ---- cross-GPU flag protocol (system scope: peers may be other GPUs) ----
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace cav
