@@ -1,7 +1,7 @@
 """ctypes mirror of include/cavity_b200.h (structs and enums only, no loading).
 
 Kept in one place so the product wrapper (`capi.py`) and the test-side
-checkers (`oracle/refbind.py`) agree on the exact C layout.
+checkers under tests agree on the exact C layout.
 """
 import ctypes as C
 

@@ -784,7 +784,8 @@ Block::~Block() {
   cudaFree(d_peer_slots);
   cudaFree(d_pack);
   cudaFree(d_unpack);
-  cudaFree(digits);
+  if (digits) cudaFreeAsync(digits, s0);
+  if (s0) cudaStreamSynchronize(s0);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (ev_a) cudaEventDestroy(ev_a);
@@ -800,7 +801,7 @@ void Block::ensure_ready() {
       throw std::logic_error("block: rank " + std::to_string(r) + " not connected (cav_block_connect)");
   std::vector<Slot*> ps(d.np);
   for (int r = 0; r < d.np; ++r) ps[r] = reinterpret_cast<Slot*>(peer_arena[r] + lay.slots);
-  CAV_CUDA(cudaMemcpy(d_peer_slots, ps.data(), d.np * sizeof(Slot*), cudaMemcpyHostToDevice));
+  CAV_CUDA(cudaMemcpyAsync(d_peer_slots, ps.data(), d.np * sizeof(Slot*), cudaMemcpyHostToDevice, s0));
   std::vector<MsgDesc> pk(plan.size()), up(plan.size());
   for (size_t m = 0; m < plan.size(); ++m) {
     const cav_plan_entry& e = plan[m];
@@ -835,9 +836,10 @@ void Block::ensure_ready() {
     up[m] = b;
   }
   if (!plan.empty()) {
-    CAV_CUDA(cudaMemcpy(d_pack, pk.data(), pk.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice));
-    CAV_CUDA(cudaMemcpy(d_unpack, up.data(), up.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice));
+    CAV_CUDA(cudaMemcpyAsync(d_pack, pk.data(), pk.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice, s0));
+    CAV_CUDA(cudaMemcpyAsync(d_unpack, up.data(), up.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice, s0));
   }
+  CAV_CUDA(cudaStreamSynchronize(s0));
   // tile shape: 32 x 8 threads, k split so the grid fills ~2 waves of 148 SMs
   const long long tiles = ((n[0] + 31) / 32) * static_cast<long long>((n[1] + 7) / 8);
   const long long want = 148 * 4;
@@ -1192,8 +1194,10 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     long long nchk = 0;
     for (long long it = first; it <= last; ++it) nchk += is_check(it);
     if (nchk > b.digits_cap) {
-      cudaFree(b.digits);
-      CAV_CUDA(cudaMalloc(&b.digits, nchk * 5 * kDigits * sizeof(unsigned long long)));
+      // stream-ordered: cudaFree/cudaMalloc may synchronise the whole device,
+      // which deadlocks against a peer rank's kernel spinning on this GPU
+      if (b.digits) CAV_CUDA(cudaFreeAsync(b.digits, b.s0));
+      CAV_CUDA(cudaMallocAsync(&b.digits, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
       b.digits_cap = nchk;
     }
     if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
@@ -1224,10 +1228,11 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     b.next_n = last + 1;
     io->n_checks = nchk;
     if (nchk && io->norm_digits)
-      CAV_CUDA(cudaMemcpy(io->norm_digits, b.digits, nchk * 5 * kDigits * sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost));
+      CAV_CUDA(cudaMemcpyAsync(io->norm_digits, b.digits, nchk * 5 * kDigits * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, b.s0));
     unsigned long long codes[2];
-    CAV_CUDA(cudaMemcpy(codes, b.err, sizeof codes, cudaMemcpyDeviceToHost));
+    CAV_CUDA(cudaMemcpyAsync(codes, b.err, sizeof codes, cudaMemcpyDeviceToHost, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
     io->err_iteration = 0;
     io->err_kind = 0;
     if (codes[1] != ~0ull) {
@@ -1261,7 +1266,8 @@ int cav_block_scalars(cav_block* bh, double* dt, double* pc) {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
     IterScalars s{};
-    CAV_CUDA(cudaMemcpy(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost));
+    CAV_CUDA(cudaMemcpyAsync(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
     *dt = s.dt;
     *pc = s.pc;
   });

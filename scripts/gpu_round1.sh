@@ -1,0 +1,13 @@
+set -x
+cd $GRAFT_REPO_ROOT
+nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke exit $?"
+timeout 1200 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?"
+timeout 300 python bench.py --steps 2000 --warmup 20 --cpu-seconds 10 > gpurun_out/bench.log 2>&1
+echo "bench exit $?"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+echo "ncu1 exit $?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step_tiled -s 5 -c 1 -o gpurun_out/prof_step python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+echo "ncu2 exit $?"

@@ -1,0 +1,59 @@
+"""The C-ABI library loads without a GPU and exports every symbol declared in
+include/*.h; the product never imports the oracle."""
+import ctypes as C
+import glob
+import os
+import re
+
+from paper_2006_02602_b200 import capi
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b(cav_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("cav_residual_box", "cav_update_box", "cav_run_case", "cav_block_create",
+                 "cav_block_run", "cav_block_connect", "cav_block_arena_ipc", "cav_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    for fmad in (False, True):
+        L = C.CDLL(capi.lib_path(fmad))
+        missing = [n for n in declared_functions() if not hasattr(L, n)]
+        assert not missing, (fmad, missing)
+
+
+def test_version_and_error_channel():
+    assert "sm_100a" in capi.version() and "fmad=false" in capi.version()
+    assert "fmad=true" in capi.version(True)
+    try:
+        capi.choose_dims(0, "3d")
+    except capi.InvalidArgument as e:
+        assert str(e) == "choose_dims: np must be >= 1"
+    else:
+        raise AssertionError("expected InvalidArgument")
+
+
+def test_product_does_not_import_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2006_02602_b200")
+    banned = re.compile(r"(from\s+oracle|import\s+oracle|refbind|libcavity_oracle|libcavity_ref|"
+                        r"cavity_oracle\.h)")
+    for path in glob.glob(os.path.join(pkg, "**", "*.*"), recursive=True):
+        if path.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp")):
+            assert not banned.search(open(path).read()), path
+
+
+def test_sm100a_cubin_in_library():
+    data = open(capi.lib_path(), "rb").read()
+    assert b"sm_100a" in data or b"sm_100" in data

@@ -10,7 +10,7 @@ import pytest
 import oracle_ops as O
 from conftest import golden_config
 from oracle.refbind import Oracle
-from paper_2006_02602_b200 import capi
+from paper_2006_02602_b200 import _abi, capi
 from paper_2006_02602_b200.capi import CavityError, InvalidArgument
 
 pytestmark = pytest.mark.gpu
@@ -55,7 +55,7 @@ def test_parallel_c0_matches_reference(golden, golden_arrays, np_, mode, strateg
     the reference's serial run (acceptance c1/c7)."""
     entry = golden["runs"]["c0_32_1000"]
     cfg = golden_config(entry, capi.default_config)
-    capi._abi.apply_overrides(cfg, np=np_, mode=mode, strategy=strategy, overlap=overlap)
+    _abi.apply_overrides(cfg, np=np_, mode=mode, strategy=strategy, overlap=overlap)
     r = capi.run_case(cfg, collect_fields=True, collect_history=True)
     check_against_golden(r, entry, golden_arrays, "c0_32_1000")
     assert r.np == np_
