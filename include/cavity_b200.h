@@ -296,6 +296,9 @@ typedef struct {
 int cav_block_run(cav_block* b, cav_run_io* io);
 /* Number of launches of this library's kernels per iteration (bench claim). */
 int cav_block_launches_per_iteration(cav_block* b, int check_iteration);
+/* Diagnostics: arena flags (64), scalar slots (np*2*8 words), error codes
+ * (2) and pack counters (64), as u64 words. */
+int cav_block_debug(cav_block* b, uint64_t* out, int cap);
 /* Last dt used and the current centre pressure shift (diagnostics). */
 int cav_block_scalars(cav_block* b, double* dt_out, double* pc_out);
 

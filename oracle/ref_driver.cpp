@@ -21,6 +21,8 @@
 #include "cavity/runner.hpp"
 #include "cavity/slab.hpp"
 #include "cavity/solver.hpp"
+#include "cavity/util/dump.hpp"
+#include "cavity/metrics.hpp"
 #include "cavity/util/repro_sum.hpp"
 #include "cavity_b200.h"
 
@@ -405,6 +407,39 @@ int ref_overlap_regions(int nx, int ny, int nz, const int rank_at[6], cav_box* i
         external[n].lo[a] = r.external[n].lo[a];
         external[n].hi[a] = r.external[n].hi[a];
       }
+  });
+}
+
+int ref_write_solution(const char* path, int nx, int ny, int nz, const double* fields) {
+  return guard([&] {
+    GlobalFields g;
+    g.size = GridSize3{nx, ny, nz};
+    const std::size_t n = g.nodes();
+    std::vector<double>* f[5] = {&g.p, &g.u, &g.v, &g.w, &g.t};
+    for (int v = 0; v < 5; ++v) f[v]->assign(fields + v * n, fields + (v + 1) * n);
+    write_solution(path, g);
+  });
+}
+
+int ref_csv_row(int np, const char* mode, const char* dims, const char* strategy, int overlap,
+                long long size, long steps, double wall, double ss, double sp, double eff,
+                unsigned long long bytes, char* out, int cap) {
+  return guard([&] {
+    metrics::RunRecord r;
+    r.np = np;
+    r.mode = mode;
+    r.dims = dims;
+    r.strategy = strategy;
+    r.overlap = overlap;
+    r.size = size;
+    r.steps = steps;
+    r.wall_time_s = wall;
+    r.ssspnt = ss;
+    r.speedup = sp;
+    r.efficiency = eff;
+    r.bytes_sent = bytes;
+    const std::string s = metrics::csv_header() + "\n" + metrics::csv_row(r);
+    std::snprintf(out, static_cast<std::size_t>(cap), "%s", s.c_str());
   });
 }
 

@@ -27,10 +27,15 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "device.cuh"
 #include "host.hpp"
 #include "ops.hpp"
 #include "status.hpp"
+#include "step_tma.cuh"
 
 namespace cav {
 
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
 // shells of src/overlap.cpp:13-28), neighbours straight from L1/L2.
 struct ShellArgs {
   StepArgs s;
+  WallInfo walls;
   int nbox;
   cav_box box[6];
   long long start[7];
@@ -352,7 +358,8 @@ __global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a
     const Geo& g = s.g;
     const long long fs = g.fstride;
     const double pc = s.sc->pc, dt = s.sc->dt;
-    const Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
+    Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
+    if (near_wall(a.walls, g, i, j, k)) apply_wall_ghosts(st, a.walls, g, i, j, k);
     const Res r = residual_of(st, s.sp);
     const double qp = st.p + dt * r.p, qu = st.u + dt * r.u, qv = st.v + dt * r.v, qw = st.w + dt * r.w,
                  qt = st.t + dt * r.t;
@@ -455,6 +462,7 @@ __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
 // small CTA, so a peer's pack can always find an SM even when several ranks
 // share one GPU (the in-process test topology).
 __global__ void __launch_bounds__(32) k_wait_flags(const XArgs a, int nmsg) {
+  if (*reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull) return;  // already failed
   for (int m = threadIdx.x; m < nmsg; m += 32) {
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(a.msg[m].flag) < static_cast<unsigned long long>(a.n)) {
@@ -532,14 +540,15 @@ __global__ void __launch_bounds__(kSyncThreads) k_scalar_sync(const SyncArgs a) 
     s->pc = mine.pc_local;
     s->err = mine.err;
     __threadfence_system();
-    st_release_sys(&s->stamp, static_cast<unsigned long long>(a.n));
+    st_release_sys(&s->stamp, static_cast<unsigned long long>(a.n) + 1);
   }
   unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
   __syncthreads();
+  const bool failed = *reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull;
   for (int r = tid; r < a.np; r += kSyncThreads) {
     const Slot* s = a.my_slots + (r * 2 + par);
     const unsigned long long t0 = globaltimer_ns();
-    while (ld_acquire_sys(&s->stamp) < static_cast<unsigned long long>(a.n)) {
+    while (!failed && ld_acquire_sys(&s->stamp) < static_cast<unsigned long long>(a.n) + 1) {
       if (globaltimer_ns() - t0 > a.timeout_ns) {
         atomicMin(a.timeout_flag, err_code(a.n, r, 15));
         break;
@@ -649,6 +658,37 @@ cudaEvent_t make_event() {
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CAV_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 4-D view (x = padded row, y, z, field) of one 5-field state for TMA; box =
+// one 36 x (TY+4) plane tile of one field.
+CUtensorMap make_state_map(const double* base, const Geo& g) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(g.ypitch),
+                              static_cast<cuuint64_t>(g.nz + 4), 5};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.pitch) * 8,
+                                 static_cast<cuuint64_t>(g.pitch) * g.ypitch * 8,
+                                 static_cast<cuuint64_t>(g.fstride) * 8};
+  const cuuint32_t box[4] = {kTmaBW, kTmaBH, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
 struct Block {
   cav_block_desc d{};
   std::array<int, 3> gn{}, dims{}, n{};
@@ -688,6 +728,10 @@ struct Block {
   std::vector<cudaEvent_t> kev;  // bench: per-step kernel timing
   int kind_ty = 8;
   int kchunk = 0;
+  CUtensorMap tmap[2];
+  WallInfo winfo{};
+  int tma_grid = 0;
+  bool use_tma = true;
 
   explicit Block(const cav_block_desc& desc);
   ~Block();
@@ -716,6 +760,9 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   host::validate_grid(n[0], n[1], n[2], dx, dy, dz);
   rank_at = host::neighbors(dims, d.rank);
   for (int f = 0; f < 6; ++f) walls[f] = rank_at[f] == CAV_WALL;
+  for (int f = 0; f < 6; ++f) winfo.wall[f] = walls[f] ? 1 : 0;
+  winfo.t_hot = d.fluid.t_hot;
+  winfo.t_cold = d.fluid.t_cold;
   const auto c = host::center_node(gn);
   owner = host::owner_of(ext, c);
   if (owner == d.rank) {
@@ -740,6 +787,19 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   for (int s = 0; s < 2; ++s) {
     CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
     CAV_CUDA(cudaMemset(state[s], 0, 5 * g.fstride * sizeof(double)));
+  }
+  for (int s = 0; s < 2; ++s) tmap[s] = make_state_map(state[s], g);
+  {
+    const char* k = std::getenv("CAV_STEP_KERNEL");
+    use_tma = !(k && std::string(k) == "tiled");
+    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kTmaSmem)));
+    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kTmaSmem)));
+    int per_sm = 0, sms = 0;
+    CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<false>, kTmaThreads, kTmaSmem));
+    CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
+    tma_grid = std::max(1, per_sm) * sms;
   }
   CAV_CUDA(cudaMalloc(&arena, lay.bytes));
   CAV_CUDA(cudaMemset(arena, 0, lay.bytes));
@@ -886,6 +946,31 @@ void Block::prologue() {
 void Block::launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig) {
   const long long vol = host::box_volume(box);
   if (vol == 0) return;
+  if (use_tma) {
+    TmaStepArgs a{};
+    a.out = state[cur ^ 1];
+    a.g = g;
+    a.sp = sp;
+    a.box = box;
+    a.sc = sc + (it & 1);
+    a.acc = acc + (it & 1);
+    a.digits = dig;
+    a.cx = cx;
+    a.cy = cy;
+    a.cz = cz;
+    a.n = it;
+    a.rank = d.rank;
+    const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
+    a.tiles_x = (bw + 31) / 32;
+    a.tiles_y = (bh + kTmaTY - 1) / kTmaTY;
+    a.total = static_cast<long long>(a.tiles_x) * a.tiles_y * bd;
+    a.walls = winfo;
+    const int grid = static_cast<int>(std::min<long long>(tma_grid, a.total));
+    if (check) k_step_tma<true><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
+    else k_step_tma<false><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
+    CAV_CUDA(cudaGetLastError());
+    return;
+  }
   StepArgs a{};
   a.in = state[cur];
   a.out = state[cur ^ 1];
@@ -924,6 +1009,7 @@ void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
   a.s.cz = cz;
   a.s.n = it;
   a.s.rank = d.rank;
+  a.walls = winfo;
   a.nbox = static_cast<int>(shells.size());
   a.start[0] = 0;
   for (int b = 0; b < a.nbox; ++b) {
@@ -939,7 +1025,7 @@ void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
 void Block::iteration(long long it, bool check, unsigned long long* dig, bool timed_kernel) {
   const IterScalars* sc_n = sc + (it & 1);
   double* f[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
-  ops::launch_bc(f, g, walls, d.fluid, sc_n, s0);
+  if (!use_tma) ops::launch_bc(f, g, walls, d.fluid, sc_n, s0);  // v1 kernel reads stored wall ghosts
   XArgs x{};
   x.state = state[cur];
   x.g = g;
@@ -1167,6 +1253,13 @@ int cav_block_download(cav_block* bh, double* host5) {
       CAV_CUDA(cudaStreamSynchronize(b.s0));
       if (b.next_n > 1) pc = s.pc;
     }
+    if (b.primed && b.next_n > 1 && b.use_tma) {
+      // ghosts the reference's BC stored at the last iteration: recompute them
+      // on the last input state with that iteration's pending shift
+      double* fp[5] = {b.field(b.cur ^ 1, 0), b.field(b.cur ^ 1, 1), b.field(b.cur ^ 1, 2), b.field(b.cur ^ 1, 3),
+                       b.field(b.cur ^ 1, 4)};
+      ops::launch_bc(fp, b.g, b.walls, b.d.fluid, b.sc + ((b.next_n - 1) & 1), b.s0);
+    }
     double* tmp = nullptr;
     CAV_CUDA(cudaMallocAsync(&tmp, 5 * S * sizeof(double), b.s0));
     k_export<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.state[b.cur], b.state[b.cur ^ 1],
@@ -1238,10 +1331,12 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     if (codes[1] != ~0ull) {
       const int kind = static_cast<int>(codes[1] & 15);
       const int who = static_cast<int>((codes[1] >> 4) & 0xFFFFF);
+      const long long tit = static_cast<long long>(codes[1] >> 24);
       throw Timeout(kind == 15 ? "transport timeout: rank " + std::to_string(b.d.rank) +
-                                     " waiting for scalars from rank " + std::to_string(who)
+                                     " waiting for scalars from rank " + std::to_string(who) + " at iteration " +
+                                     std::to_string(tit)
                                : "transport timeout: rank " + std::to_string(b.d.rank) + " waiting on face " +
-                                     std::to_string(kind - 8));
+                                     std::to_string(kind - 8) + " at iteration " + std::to_string(tit));
     }
     if (codes[0] != ~0ull && static_cast<long long>(codes[0] >> 24) <= last) {
       io->err_iteration = static_cast<long long>(codes[0] >> 24);
@@ -1251,12 +1346,28 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
   });
 }
 
+int cav_block_debug(cav_block* bh, uint64_t* out, int cap) {
+  return guarded([&] {
+    Block& b = *bh->b;
+    CAV_CUDA(cudaSetDevice(b.d.device));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s1));
+    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64);
+    CAV_CUDA(cudaMemcpy(v.data(), b.arena, (64 + 16 * b.d.np) * 8, cudaMemcpyDeviceToHost));
+    CAV_CUDA(cudaMemcpy(v.data() + 64 + 16 * b.d.np, b.err, 16, cudaMemcpyDeviceToHost));
+    std::vector<unsigned> c(64);
+    CAV_CUDA(cudaMemcpy(c.data(), b.counters, 64 * 4, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < 64; ++q) v[66 + 16 * b.d.np + q] = c[q];
+    for (size_t q = 0; q < v.size() && static_cast<int>(q) < cap; ++q) out[q] = v[q];
+  });
+}
+
 int cav_block_launches_per_iteration(cav_block* bh, int check) {
   Block& b = *bh->b;
   (void)check;
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
-  int n = (walls ? 1 : 0) + 1 + 1;  // bc, step, sync
+  int n = (walls && !b.use_tma ? 1 : 0) + 1 + 1;  // [bc], step, sync
   if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);
   return n;
 }

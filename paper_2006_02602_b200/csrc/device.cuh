@@ -81,6 +81,98 @@ __device__ __forceinline__ Star load_star(const double* __restrict__ P, const do
   return s;
 }
 
+// Wall ghosts on the fly (apply_boundary_conditions, src/solver.cpp:158-191):
+// a cell next to a wall face gets the ghost values the reference's BC pass
+// would have stored, computed from the same (lazily shifted) interior values
+// the star already holds, so no separate BC pass touches HBM.
+//   u,v,w: g0 = -i0;  T: g0 = 2*t_wall - i0 (x walls) or i0 (y, z walls)
+//   p: g0 = (3*i0 - 3*i1) + i2,  g1 = (3*g0 - 3*i0) + i1
+struct WallInfo {
+  unsigned char wall[6];
+  double t_hot, t_cold;
+};
+
+__device__ __forceinline__ double cubic_g0(double i0, double i1, double i2) { return (3.0 * i0 - 3.0 * i1) + i2; }
+__device__ __forceinline__ double cubic_g1(double g0, double i0, double i1) { return (3.0 * g0 - 3.0 * i0) + i1; }
+
+__device__ __forceinline__ void apply_wall_ghosts(Star& s, const WallInfo& w, const Geo& g, int i, int j, int k) {
+  // x walls (isothermal)
+  if (w.wall[0] && i == 2) {
+    const double g0 = cubic_g0(s.p, s.pxp, s.pxp2);
+    s.pxm2 = cubic_g1(g0, s.p, s.pxp);
+    s.pxm = g0;
+    s.uxm = -s.u;
+    s.vxm = -s.v;
+    s.wxm = -s.w;
+    s.txm = 2.0 * w.t_hot - s.t;
+  } else if (w.wall[0] && i == 3) {
+    s.pxm2 = cubic_g0(s.pxm, s.p, s.pxp);
+  }
+  if (w.wall[1] && i == g.nx + 1) {
+    const double g0 = cubic_g0(s.p, s.pxm, s.pxm2);
+    s.pxp2 = cubic_g1(g0, s.p, s.pxm);
+    s.pxp = g0;
+    s.uxp = -s.u;
+    s.vxp = -s.v;
+    s.wxp = -s.w;
+    s.txp = 2.0 * w.t_cold - s.t;
+  } else if (w.wall[1] && i == g.nx) {
+    s.pxp2 = cubic_g0(s.pxp, s.p, s.pxm);
+  }
+  // y walls (adiabatic)
+  if (w.wall[2] && j == 2) {
+    const double g0 = cubic_g0(s.p, s.pyp, s.pyp2);
+    s.pym2 = cubic_g1(g0, s.p, s.pyp);
+    s.pym = g0;
+    s.uym = -s.u;
+    s.vym = -s.v;
+    s.wym = -s.w;
+    s.tym = s.t;
+  } else if (w.wall[2] && j == 3) {
+    s.pym2 = cubic_g0(s.pym, s.p, s.pyp);
+  }
+  if (w.wall[3] && j == g.ny + 1) {
+    const double g0 = cubic_g0(s.p, s.pym, s.pym2);
+    s.pyp2 = cubic_g1(g0, s.p, s.pym);
+    s.pyp = g0;
+    s.uyp = -s.u;
+    s.vyp = -s.v;
+    s.wyp = -s.w;
+    s.typ = s.t;
+  } else if (w.wall[3] && j == g.ny) {
+    s.pyp2 = cubic_g0(s.pyp, s.p, s.pym);
+  }
+  // z walls (adiabatic)
+  if (w.wall[4] && k == 2) {
+    const double g0 = cubic_g0(s.p, s.pzp, s.pzp2);
+    s.pzm2 = cubic_g1(g0, s.p, s.pzp);
+    s.pzm = g0;
+    s.uzm = -s.u;
+    s.vzm = -s.v;
+    s.wzm = -s.w;
+    s.tzm = s.t;
+  } else if (w.wall[4] && k == 3) {
+    s.pzm2 = cubic_g0(s.pzm, s.p, s.pzp);
+  }
+  if (w.wall[5] && k == g.nz + 1) {
+    const double g0 = cubic_g0(s.p, s.pzm, s.pzm2);
+    s.pzp2 = cubic_g1(g0, s.p, s.pzm);
+    s.pzp = g0;
+    s.uzp = -s.u;
+    s.vzp = -s.v;
+    s.wzp = -s.w;
+    s.tzp = s.t;
+  } else if (w.wall[5] && k == g.nz) {
+    s.pzp2 = cubic_g0(s.pzp, s.p, s.pzm);
+  }
+}
+
+// true when the cell touches a wall's two-layer ghost band on any axis
+__device__ __forceinline__ bool near_wall(const WallInfo& w, const Geo& g, int i, int j, int k) {
+  return (w.wall[0] && i <= 3) || (w.wall[1] && i >= g.nx) || (w.wall[2] && j <= 3) ||
+         (w.wall[3] && j >= g.ny) || (w.wall[4] && k <= 3) || (w.wall[5] && k >= g.nz);
+}
+
 // Block-wide max of three doubles and OR of a mask; thread 0 gets the result.
 template <int NT>
 __device__ __forceinline__ void block_reduce_max3_or(double& a, double& b, double& c, unsigned& m) {
