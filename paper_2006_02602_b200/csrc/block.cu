@@ -788,6 +788,22 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
     CAV_CUDA(cudaMemset(state[s], 0, 5 * g.fstride * sizeof(double)));
   }
+  {  // load every kernel module now (see ops::preload_kernels)
+    ops::preload_kernels();
+    cudaFuncAttributes fa;
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, false>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, true>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<false>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<true>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<false>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<true>));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_pack));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_wait_flags));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_unpack));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_scalar_sync));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
+  }
   for (int s = 0; s < 2; ++s) tmap[s] = make_state_map(state[s], g);
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");

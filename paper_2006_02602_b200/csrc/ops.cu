@@ -253,6 +253,17 @@ void update_box(double* q, const double* r, double dt, int X, int Y, const cav_b
   CAV_CUDA(cudaGetLastError());
 }
 
+void preload_kernels() {
+  cudaFuncAttributes fa;
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_residual_box));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_update_box));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_rescale));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_copy_box));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_dt_scan));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_norm_digits));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_bc));
+}
+
 void launch_dt_scan(const cav_field_ptrs& f, const Geo& g, const cav_box& box, double u_ref, Acc* acc,
                     long long it_no, int rank, cudaStream_t st) {
   const BoxIter it = box_iter(box);

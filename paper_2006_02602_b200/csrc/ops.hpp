@@ -25,6 +25,12 @@ void launch_bc(double* const fields[5], const Geo& g, const int walls[6], const 
 void launch_dt_scan(const cav_field_ptrs& f, const Geo& g, const cav_box& box, double u_ref, Acc* acc,
                     long long it_no, int rank, cudaStream_t st);
 
+// Forces every op-level kernel's module to load now. CUDA lazy loading would
+// otherwise load a kernel at its first launch, which needs a context-wide
+// synchronisation that can deadlock against a peer rank's spinning kernel on
+// the same GPU.
+void preload_kernels();
+
 // dt = cfl * min(min(dx/Du, dy/Dv, dz/Dw), visc, therm) from the exact maxima
 // of the CFL denominators (src/solver.cpp:215-231 with the max rewrite).
 __host__ __device__ inline double dt_from_maxima(const unsigned long long dmax[3], double dx, double dy,
