@@ -27,6 +27,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# several ranks may share one GPU when testing the multi-process path on one device
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "cell-updates/s (MCUPS) at 1/2/4/8 B200, % HBM roofline, vs CPU ref"
 UNIT = "MCUPS"

@@ -17,6 +17,11 @@ import numpy as np
 
 from . import _abi as A
 
+# Several in-process ranks may share one GPU (tests); each drives two streams
+# whose kernels wait on each other, so the streams must not share hardware
+# queues. Effective only if set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_NAME = "libcavity_b200.so"
 LIB_FMAD_NAME = "libcavity_b200_fmad.so"

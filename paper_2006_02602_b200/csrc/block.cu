@@ -812,6 +812,8 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
                                   static_cast<int>(kTmaSmem)));
     CAV_CUDA(cudaFuncSetAttribute(k_step_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kTmaSmem)));
+    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int per_sm = 0, sms = 0;
     CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<false>, kTmaThreads, kTmaSmem));
     CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
@@ -978,10 +980,24 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.rank = d.rank;
     const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
     a.tiles_x = (bw + 31) / 32;
-    a.tiles_y = (bh + kTmaTY - 1) / kTmaTY;
-    a.total = static_cast<long long>(a.tiles_x) * a.tiles_y * bd;
+    a.ntiles = a.tiles_x * ((bh + kTmaTY - 1) / kTmaTY);
+    // k-chunk: balance items over the persistent grid (rounds/ceil(rounds))
+    // while keeping the per-item window restart (4 extra planes) small
+    double best = -1.0;
+    for (int L = std::min(bd, 64); L >= std::min(bd, 8); --L) {
+      const long long items = static_cast<long long>(a.ntiles) * ((bd + L - 1) / L);
+      const double rounds = static_cast<double>(items) / tma_grid;
+      const double eff = rounds / std::ceil(rounds);
+      const double score = eff * static_cast<double>(L) / (L + 2.0);
+      if (score > best + 1e-9) {
+        best = score;
+        a.chunk = L;
+      }
+    }
+    a.nchunks = (bd + a.chunk - 1) / a.chunk;
     a.walls = winfo;
-    const int grid = static_cast<int>(std::min<long long>(tma_grid, a.total));
+    const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
+    const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
     if (check) k_step_tma<true><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
     else k_step_tma<false><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
     CAV_CUDA(cudaGetLastError());

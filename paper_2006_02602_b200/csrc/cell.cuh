@@ -32,58 +32,97 @@ struct Res {
   double p, u, v, w, t;
 };
 
-// residual_cell, value form (kernels_cell.hpp:22-78).
-__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q) {
-  const double uc = s.u, vc = s.v, wc = s.w, tc = s.t;
+// residual_cell (kernels_cell.hpp:22-78), written once against an accessor S
+// that yields the star's values (S::p(), S::pxm(), ...). Every expression and
+// its parenthesisation is the reference's; only the order in which independent
+// expressions are evaluated is grouped per equation, which keeps fewer values
+// live and cannot change any result.
+template <class S>
+__device__ __forceinline__ Res residual_t(const S& s, const cav_stencil_params& q) {
+  const double uc = s.u(), vc = s.v(), wc = s.w(), tc = s.t();
   const double speed = sqrt((uc * uc + vc * vc) + wc * wc);
   const double b = smax(speed, q.u_ref);
   const double b2 = b * b;
-
-  const double ux = (s.uxp - s.uxm) * q.inv2dx;
-  const double uy = (s.uyp - s.uym) * q.inv2dy;
-  const double uz = (s.uzp - s.uzm) * q.inv2dz;
-  const double vx = (s.vxp - s.vxm) * q.inv2dx;
-  const double vy = (s.vyp - s.vym) * q.inv2dy;
-  const double vz = (s.vzp - s.vzm) * q.inv2dz;
-  const double wx = (s.wxp - s.wxm) * q.inv2dx;
-  const double wy = (s.wyp - s.wym) * q.inv2dy;
-  const double wz = (s.wzp - s.wzm) * q.inv2dz;
-  const double tx = (s.txp - s.txm) * q.inv2dx;
-  const double ty = (s.typ - s.tym) * q.inv2dy;
-  const double tz = (s.tzp - s.tzm) * q.inv2dz;
-  const double px = (s.pxp - s.pxm) * q.inv2dx;
-  const double py = (s.pyp - s.pym) * q.inv2dy;
-  const double pz = (s.pzp - s.pzm) * q.inv2dz;
-
   Res r;
+  // continuity + fourth-difference damping
+  const double ux = (s.uxp() - s.uxm()) * q.inv2dx;
+  const double vy = (s.vyp() - s.vym()) * q.inv2dy;
+  const double wz = (s.wzp() - s.wzm()) * q.inv2dz;
   const double dv = (ux + vy) + wz;
-  const double p6 = 6.0 * s.p;
-  const double fx = ((((s.pxm2 - 4.0 * s.pxm) + p6) - 4.0 * s.pxp) + s.pxp2) * q.invdx4;
-  const double fy = ((((s.pym2 - 4.0 * s.pym) + p6) - 4.0 * s.pyp) + s.pyp2) * q.invdy4;
-  const double fz = ((((s.pzm2 - 4.0 * s.pzm) + p6) - 4.0 * s.pzp) + s.pzp2) * q.invdz4;
+  const double pc = s.p();
+  const double p6 = 6.0 * pc;
+  const double pxm = s.pxm(), pxp = s.pxp();
+  const double fx = ((((s.pxm2() - 4.0 * pxm) + p6) - 4.0 * pxp) + s.pxp2()) * q.invdx4;
+  const double px = (pxp - pxm) * q.inv2dx;
+  const double pym = s.pym(), pyp = s.pyp();
+  const double fy = ((((s.pym2() - 4.0 * pym) + p6) - 4.0 * pyp) + s.pyp2()) * q.invdy4;
+  const double py = (pyp - pym) * q.inv2dy;
+  const double pzm = s.pzm(), pzp = s.pzp();
+  const double fz = ((((s.pzm2() - 4.0 * pzm) + p6) - 4.0 * pzp) + s.pzp2()) * q.invdz4;
+  const double pz = (pzp - pzm) * q.inv2dz;
   const double dmp = b * ((q.kdx3 * fx + q.kdy3 * fy) + q.kdz3 * fz);
   r.p = -b2 * (q.rho * dv + dmp);
-
-  const double u2 = 2.0 * uc, v2 = 2.0 * vc, w2 = 2.0 * wc, t2 = 2.0 * tc;
-  const double lu = ((s.uxp - u2) + s.uxm) * q.invdx2 + ((s.uyp - u2) + s.uym) * q.invdy2 +
-                    ((s.uzp - u2) + s.uzm) * q.invdz2;
-  const double lv = ((s.vxp - v2) + s.vxm) * q.invdx2 + ((s.vyp - v2) + s.vym) * q.invdy2 +
-                    ((s.vzp - v2) + s.vzm) * q.invdz2;
-  const double lw = ((s.wxp - w2) + s.wxm) * q.invdx2 + ((s.wyp - w2) + s.wym) * q.invdy2 +
-                    ((s.wzp - w2) + s.wzm) * q.invdz2;
-  const double cu = (uc * ux + vc * uy) + wc * uz;
-  const double cv = (uc * vx + vc * vy) + wc * vz;
-  const double cw = (uc * wx + vc * wy) + wc * wz;
   const double by = q.sigma * (tc - q.t_inf);
-  r.u = ((-cu - q.inv_rho * px) + q.nu * lu) + by * q.gx;
-  r.v = ((-cv - q.inv_rho * py) + q.nu * lv) + by * q.gy;
-  r.w = ((-cw - q.inv_rho * pz) + q.nu * lw) + by * q.gz;
-
-  const double lt = ((s.txp - t2) + s.txm) * q.invdx2 + ((s.typ - t2) + s.tym) * q.invdy2 +
-                    ((s.tzp - t2) + s.tzm) * q.invdz2;
-  const double ct = (uc * tx + vc * ty) + wc * tz;
-  r.t = -ct + q.alpha * lt;
+  // x momentum
+  {
+    const double uxm = s.uxm(), uxp = s.uxp(), uym = s.uym(), uyp = s.uyp(), uzm = s.uzm(), uzp = s.uzp();
+    const double uy = (uyp - uym) * q.inv2dy;
+    const double uz = (uzp - uzm) * q.inv2dz;
+    const double u2 = 2.0 * uc;
+    const double lu = ((uxp - u2) + uxm) * q.invdx2 + ((uyp - u2) + uym) * q.invdy2 + ((uzp - u2) + uzm) * q.invdz2;
+    const double cu = (uc * ux + vc * uy) + wc * uz;
+    r.u = ((-cu - q.inv_rho * px) + q.nu * lu) + by * q.gx;
+  }
+  // y momentum
+  {
+    const double vxm = s.vxm(), vxp = s.vxp(), vym = s.vym(), vyp = s.vyp(), vzm = s.vzm(), vzp = s.vzp();
+    const double vx = (vxp - vxm) * q.inv2dx;
+    const double vz = (vzp - vzm) * q.inv2dz;
+    const double v2 = 2.0 * vc;
+    const double lv = ((vxp - v2) + vxm) * q.invdx2 + ((vyp - v2) + vym) * q.invdy2 + ((vzp - v2) + vzm) * q.invdz2;
+    const double cv = (uc * vx + vc * vy) + wc * vz;
+    r.v = ((-cv - q.inv_rho * py) + q.nu * lv) + by * q.gy;
+  }
+  // z momentum
+  {
+    const double wxm = s.wxm(), wxp = s.wxp(), wym = s.wym(), wyp = s.wyp(), wzm = s.wzm(), wzp = s.wzp();
+    const double wx = (wxp - wxm) * q.inv2dx;
+    const double wy = (wyp - wym) * q.inv2dy;
+    const double w2 = 2.0 * wc;
+    const double lw = ((wxp - w2) + wxm) * q.invdx2 + ((wyp - w2) + wym) * q.invdy2 + ((wzp - w2) + wzm) * q.invdz2;
+    const double cw = (uc * wx + vc * wy) + wc * wz;
+    r.w = ((-cw - q.inv_rho * pz) + q.nu * lw) + by * q.gz;
+  }
+  // energy
+  {
+    const double txm = s.txm(), txp = s.txp(), tym = s.tym(), typ = s.typ(), tzm = s.tzm(), tzp = s.tzp();
+    const double tx = (txp - txm) * q.inv2dx;
+    const double ty = (typ - tym) * q.inv2dy;
+    const double tz = (tzp - tzm) * q.inv2dz;
+    const double t2 = 2.0 * tc;
+    const double lt = ((txp - t2) + txm) * q.invdx2 + ((typ - t2) + tym) * q.invdy2 + ((tzp - t2) + tzm) * q.invdz2;
+    const double ct = (uc * tx + vc * ty) + wc * tz;
+    r.t = -ct + q.alpha * lt;
+  }
   return r;
+}
+
+// Accessor over a Star value (pointwise kernels).
+struct StarAcc {
+  const Star& s;
+#define CAV_A(n) \
+  __device__ __forceinline__ double n() const { return s.n; }
+  CAV_A(p) CAV_A(pxm) CAV_A(pxp) CAV_A(pxm2) CAV_A(pxp2) CAV_A(pym) CAV_A(pyp) CAV_A(pym2) CAV_A(pyp2)
+  CAV_A(pzm) CAV_A(pzp) CAV_A(pzm2) CAV_A(pzp2)
+  CAV_A(u) CAV_A(uxm) CAV_A(uxp) CAV_A(uym) CAV_A(uyp) CAV_A(uzm) CAV_A(uzp)
+  CAV_A(v) CAV_A(vxm) CAV_A(vxp) CAV_A(vym) CAV_A(vyp) CAV_A(vzm) CAV_A(vzp)
+  CAV_A(w) CAV_A(wxm) CAV_A(wxp) CAV_A(wym) CAV_A(wyp) CAV_A(wzm) CAV_A(wzp)
+  CAV_A(t) CAV_A(txm) CAV_A(txp) CAV_A(tym) CAV_A(typ) CAV_A(tzm) CAV_A(tzp)
+#undef CAV_A
+};
+
+__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q) {
+  return residual_t(StarAcc{s}, q);
 }
 
 // compute_beta (include/cavity/solver.hpp:73-75) and the per-cell CFL

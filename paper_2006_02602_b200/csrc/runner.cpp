@@ -9,6 +9,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -228,6 +229,21 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
     if (cfg->np < 1 || cfg->np > 512) throw std::invalid_argument("run: np must be in 1..512");
     const auto dims = host::decomp_dims(cfg->np, cfg->mode, cfg->dims);
     host::cavity_spacing(cfg->nx, cfg->ny, cfg->nz, cfg->fluid.length, cfg->fluid.length, cfg->fluid.length);
+    // Ranks sharing a GPU each drive 2 streams whose spinning kernels wait on
+    // each other; CUDA multiplexes streams onto CUDA_DEVICE_MAX_CONNECTIONS
+    // hardware queues (default 8), and two streams on one queue would
+    // serialise a waiter ahead of the kernel it waits for.
+    {
+      int per_dev[8] = {};
+      for (int r = 0; r < cfg->np; ++r) ++per_dev[cfg->devices[r % 8] & 7];
+      int most = 0;
+      for (int d = 0; d < 8; ++d) most = std::max(most, per_dev[d]);
+      const char* env = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+      const int conns = env ? std::atoi(env) : 8;
+      if (most > 1 && 2 * most > conns)
+        throw std::invalid_argument("run: " + std::to_string(most) + " ranks share one GPU; set CUDA_DEVICE_MAX_CONNECTIONS >= " +
+                                    std::to_string(2 * most) + " (max 32) before CUDA initialises");
+    }
     Shared sh(cfg, opt, cfg->np);
     sh.gn = {cfg->nx, cfg->ny, cfg->nz};
     sh.dims = dims;

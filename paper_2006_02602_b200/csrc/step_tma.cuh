@@ -1,21 +1,27 @@
-// step_tma.cuh — the fused pseudo-time step (K4) fed by TMA.
+// step_tma.cuh — the fused pseudo-time step (K4), TMA-fed and warp-specialised.
 //
-// One CTA = 1 producer warp + TY consumer warps (32 x TY cells per plane).
-// The producer streams 36 x (TY+4) plane tiles of all five fields (the tile
-// plus a 2-cell halo ring; corners ride along and are never read) into a ring
-// of R shared-memory slots with cp.async.bulk.tensor, completion tracked by
-// mbarrier transaction counts. Consumers keep their own column's k-window in
-// registers (p: k-2..k+2, u,v,w,T: k-1..k+1), read in-plane neighbours from
-// the slot of plane k, and release a slot through an `empty` mbarrier when no
-// later step needs it. There is no CTA-wide barrier per plane.
+// One persistent CTA per SM: 1 producer warp + TY consumer warps (a 32 x TY
+// tile of cells per plane, one cell per consumer thread).
 //
-// Work: the (tile, plane) space of the box is linearised tile-major and split
-// evenly over a grid of exactly `ctas_per_sm x #SMs` CTAs; each CTA walks one
-// or two contiguous segments (a segment restarts the k-window), so every SM
-// gets the same number of cell updates (no wave tail).
+// Producer warp: streams 36 x (TY+4) plane tiles of all five fields (tile plus
+// a 2-cell halo ring) into a ring of R shared-memory slots with
+// cp.async.bulk.tensor.4d (completion = mbarrier transaction count). LAG
+// entries behind the issue front it finalises each landed plane in place —
+// the lazy rescale fl(p - pc) on interior pressure, and the wall ghosts of
+// apply_boundary_conditions (src/solver.cpp:158-191) for x/y walls — and
+// arrives on the slot's `ready` mbarrier. So consumers read final values only.
 //
-// Arithmetic per cell is residual_of() from cell.cuh — identical to the
-// pointwise kernels — so results are bitwise those of the reference.
+// Consumer warps: keep their column's k-window in registers (p: k-2..k+2,
+// u,v,w,T: k-1..k+1; z-wall ghosts are formed there), read in-plane
+// neighbours from the ready slot of plane k, compute residual_t (cell.cuh,
+// the reference's arithmetic), the Euler update, the next step's CFL maxima
+// and the non-finite flags, store, and release the slot (`empty` mbarrier).
+// There is no CTA-wide barrier per plane.
+//
+// Work: items are (k-chunk, tile) in chunk-major order; CTA c takes items
+// c, c+G, c+2G, ... so the ~G items in flight at any time are neighbouring
+// tiles of the same chunk: their halo rows are L2 hits, every SM gets the same
+// number of items (+-1), and each item restarts the k-window once.
 #pragma once
 
 #include <cuda.h>
@@ -59,11 +65,24 @@ __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int x
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(f), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void consumer_sync(int nthreads) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace tma
+
+constexpr int kTmaTY = 16;                              // consumer warps = tile rows
+constexpr int kTmaRing = 7;                             // plane slots
+constexpr int kTmaLag = 3;                              // patch lag behind the TMA front
+constexpr int kTmaBW = 36;                              // 32 + 2x2 halo
+constexpr int kTmaBH = kTmaTY + 4;
+constexpr int kTmaField = kTmaBW * kTmaBH;              // doubles per field plane
+constexpr int kTmaSlot = 5 * kTmaField;                 // doubles per slot
+constexpr int kTmaThreads = 32 * (kTmaTY + 1);
+constexpr size_t kTmaSmem = kTmaRing * kTmaSlot * sizeof(double) + 3 * kTmaRing * 8 + 5 * kDigits * 8;
+static_assert(kTmaField * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
+static_assert(kTmaRing >= kTmaLag + 4, "ring too small for the patch lag (deadlock)");
 
 struct TmaStepArgs {
   double* out;
@@ -76,34 +95,154 @@ struct TmaStepArgs {
   int cx, cy, cz;
   long long n;
   int rank;
-  int tiles_x, tiles_y;
-  long long total;  // tiles * depth
-  WallInfo walls;   // wall ghosts are computed in-kernel (no BC pass)
+  int tiles_x, ntiles, chunk, nchunks;
+  WallInfo walls;
 };
 
-constexpr int kTmaTY = 8;          // consumer warps per CTA / tile rows
-constexpr int kTmaRing = 6;        // plane slots
-constexpr int kTmaBW = 36;         // 32 + 2x2 halo
-constexpr int kTmaBH = kTmaTY + 4;
-constexpr int kTmaField = kTmaBW * kTmaBH;            // doubles per field plane
-constexpr int kTmaSlot = 5 * kTmaField;               // doubles per slot
-constexpr int kTmaThreads = 32 * (kTmaTY + 1);
-constexpr size_t kTmaSmem = kTmaRing * kTmaSlot * sizeof(double) + 3 * kTmaRing * 8 + 5 * kDigits * 8 + 128;
+struct ItemGeom {
+  int ti0, tj0, kb, ke;
+};
+
+__device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long item) {
+  const int chunk = static_cast<int>(item / a.ntiles);
+  const int tile = static_cast<int>(item % a.ntiles);
+  ItemGeom r;
+  r.ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
+  r.tj0 = a.box.lo[1] + (tile / a.tiles_x) * kTmaTY;
+  r.kb = a.box.lo[2] + chunk * a.chunk;
+  r.ke = min(r.kb + a.chunk, a.box.hi[2]);
+  return r;
+}
+
+// Consumer-side star accessor: in-plane neighbours from the ready slot,
+// k-neighbours from the register window.
+struct SmemAcc {
+  const double *P, *U, *V, *W, *T;
+  double pc_, pzm_, pzp_, pzm2_, pzp2_;
+  double u_, uzm_, uzp_, v_, vzm_, vzp_, w_, wzm_, wzp_, t_, tzm_, tzp_;
+  __device__ __forceinline__ double p() const { return pc_; }
+  __device__ __forceinline__ double pxm() const { return P[-1]; }
+  __device__ __forceinline__ double pxp() const { return P[1]; }
+  __device__ __forceinline__ double pxm2() const { return P[-2]; }
+  __device__ __forceinline__ double pxp2() const { return P[2]; }
+  __device__ __forceinline__ double pym() const { return P[-kTmaBW]; }
+  __device__ __forceinline__ double pyp() const { return P[kTmaBW]; }
+  __device__ __forceinline__ double pym2() const { return P[-2 * kTmaBW]; }
+  __device__ __forceinline__ double pyp2() const { return P[2 * kTmaBW]; }
+  __device__ __forceinline__ double pzm() const { return pzm_; }
+  __device__ __forceinline__ double pzp() const { return pzp_; }
+  __device__ __forceinline__ double pzm2() const { return pzm2_; }
+  __device__ __forceinline__ double pzp2() const { return pzp2_; }
+#define CAV_Q(F, A)                                                                       \
+  __device__ __forceinline__ double F() const { return F##_; }                           \
+  __device__ __forceinline__ double F##xm() const { return A[-1]; }                      \
+  __device__ __forceinline__ double F##xp() const { return A[1]; }                       \
+  __device__ __forceinline__ double F##ym() const { return A[-kTmaBW]; }                 \
+  __device__ __forceinline__ double F##yp() const { return A[kTmaBW]; }                  \
+  __device__ __forceinline__ double F##zm() const { return F##zm_; }                     \
+  __device__ __forceinline__ double F##zp() const { return F##zp_; }
+  CAV_Q(u, U)
+  CAV_Q(v, V)
+  CAV_Q(w, W)
+  CAV_Q(t, T)
+#undef CAV_Q
+};
+
+// Producer: finalise one landed plane tile in shared memory (all 32 lanes).
+__device__ __forceinline__ void patch_plane(double* slot, const TmaStepArgs& a, const ItemGeom& it, int pl,
+                                            double pc, int lane) {
+  const Geo& g = a.g;
+  if (pl < 2 || pl >= g.nz + 2) return;  // ghost planes: read only as column values
+  double* P = slot;
+  const int i0 = it.ti0 - 2, j0 = it.tj0 - 2;
+  // lazy rescale of interior pressure (rescale_pressure, src/solver.cpp:248-257)
+  for (int e = lane; e < kTmaField; e += 32) {
+    const int x = e % kTmaBW, y = e / kTmaBW;
+    const int i = i0 + x, j = j0 + y;
+    if (i >= 2 && i < g.nx + 2 && j >= 2 && j < g.ny + 2) P[e] = P[e] - pc;
+  }
+  __syncwarp();
+  const WallInfo& w = a.walls;
+  double* U = slot + kTmaField;
+  double* V = U + kTmaField;
+  double* W = V + kTmaField;
+  double* T = W + kTmaField;
+  // x walls: ghost columns for rows with interior j
+  if (w.wall[0] && i0 == 0) {
+    for (int y = lane; y < kTmaBH; y += 32) {
+      const int j = j0 + y;
+      if (j < 2 || j >= g.ny + 2) continue;
+      const int r = y * kTmaBW;
+      const double g0 = cubic_g0(P[r + 2], P[r + 3], P[r + 4]);
+      P[r + 1] = g0;
+      P[r] = cubic_g1(g0, P[r + 2], P[r + 3]);
+      U[r + 1] = -U[r + 2];
+      V[r + 1] = -V[r + 2];
+      W[r + 1] = -W[r + 2];
+      T[r + 1] = 2.0 * w.t_hot - T[r + 2];
+    }
+  }
+  const int xg = g.nx + 2 - i0;  // tile column of the high x ghost g0
+  if (w.wall[1] && xg >= 3 && xg < kTmaBW) {
+    for (int y = lane; y < kTmaBH; y += 32) {
+      const int j = j0 + y;
+      if (j < 2 || j >= g.ny + 2) continue;
+      const int r = y * kTmaBW;
+      const double g0 = cubic_g0(P[r + xg - 1], P[r + xg - 2], P[r + xg - 3]);
+      P[r + xg] = g0;
+      if (xg + 1 < kTmaBW) P[r + xg + 1] = cubic_g1(g0, P[r + xg - 1], P[r + xg - 2]);
+      U[r + xg] = -U[r + xg - 1];
+      V[r + xg] = -V[r + xg - 1];
+      W[r + xg] = -W[r + xg - 1];
+      T[r + xg] = 2.0 * w.t_cold - T[r + xg - 1];
+    }
+  }
+  // y walls: ghost rows for columns with interior i
+  if (w.wall[2] && j0 == 0) {
+    for (int x = lane; x < kTmaBW; x += 32) {
+      const int i = i0 + x;
+      if (i < 2 || i >= g.nx + 2) continue;
+      const double g0 = cubic_g0(P[2 * kTmaBW + x], P[3 * kTmaBW + x], P[4 * kTmaBW + x]);
+      P[kTmaBW + x] = g0;
+      P[x] = cubic_g1(g0, P[2 * kTmaBW + x], P[3 * kTmaBW + x]);
+      U[kTmaBW + x] = -U[2 * kTmaBW + x];
+      V[kTmaBW + x] = -V[2 * kTmaBW + x];
+      W[kTmaBW + x] = -W[2 * kTmaBW + x];
+      T[kTmaBW + x] = T[2 * kTmaBW + x];
+    }
+  }
+  const int yg = g.ny + 2 - j0;
+  if (w.wall[3] && yg >= 3 && yg < kTmaBH) {
+    for (int x = lane; x < kTmaBW; x += 32) {
+      const int i = i0 + x;
+      if (i < 2 || i >= g.nx + 2) continue;
+      const double g0 = cubic_g0(P[(yg - 1) * kTmaBW + x], P[(yg - 2) * kTmaBW + x], P[(yg - 3) * kTmaBW + x]);
+      P[yg * kTmaBW + x] = g0;
+      if (yg + 1 < kTmaBH) P[(yg + 1) * kTmaBW + x] = cubic_g1(g0, P[(yg - 1) * kTmaBW + x], P[(yg - 2) * kTmaBW + x]);
+      U[yg * kTmaBW + x] = -U[(yg - 1) * kTmaBW + x];
+      V[yg * kTmaBW + x] = -V[(yg - 1) * kTmaBW + x];
+      W[yg * kTmaBW + x] = -W[(yg - 1) * kTmaBW + x];
+      T[yg * kTmaBW + x] = T[(yg - 1) * kTmaBW + x];
+    }
+  }
+}
 
 template <bool NORMS>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(kTmaThreads, 1)
     k_step_tma(const __grid_constant__ CUtensorMap map, const TmaStepArgs a) {
-  constexpr int TY = kTmaTY, C = kTmaTY, R = kTmaRing, BW = kTmaBW;
+  constexpr int C = kTmaTY, R = kTmaRing, BW = kTmaBW;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + R * kTmaSlot * sizeof(double));
-  uint64_t* empty = full + R;
-  unsigned long long* sdig = reinterpret_cast<unsigned long long*>(empty + 2 * R);
+  uint64_t* ready = full + R;
+  uint64_t* empty = ready + R;
+  unsigned long long* sdig = reinterpret_cast<unsigned long long*>(empty + R);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {
       tma::mbar_init(&full[s], 1);
+      tma::mbar_init(&ready[s], 1);
       tma::mbar_init(&empty[s], C);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -112,30 +251,54 @@ __global__ void __maxnreg__(112)
     for (int x = threadIdx.x; x < 5 * kDigits; x += kTmaThreads) sdig[x] = 0;
   __syncthreads();
 
-  const int bd = a.box.hi[2] - a.box.lo[2];
-  const long long u0 = a.total * blockIdx.x / gridDim.x;
-  const long long u1 = a.total * (blockIdx.x + 1) / gridDim.x;
+  const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
+  const long long G = gridDim.x;
+  const double pc = a.sc->pc;
 
   if (warp == C) {
     // ---------------- producer ----------------
-    if (lane == 0) {
-      uint32_t e = 0;
-      for (long long u = u0; u < u1;) {
-        const int tile = static_cast<int>(u / bd);
-        const int kb = a.box.lo[2] + static_cast<int>(u % bd);
-        const long long rem_ = bd - u % bd;
-        const int len = static_cast<int>(rem_ < u1 - u ? rem_ : u1 - u);
-        const int ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
-        const int tj0 = a.box.lo[1] + (tile / a.tiles_x) * TY;
-        for (int pl = kb - 2; pl <= kb + len + 1; ++pl, ++e) {
-          const int s = e % R;
+    long long it_i = blockIdx.x, it_p = blockIdx.x;  // issue / patch cursors (items)
+    ItemGeom gi{0, 0, 0, 0};
+    if (it_i < total) gi = item_geom(a, it_i);
+    ItemGeom gp = gi;
+    int pl_i = gi.kb - 2, pl_p = gi.kb - 2;
+    uint32_t ep = 0;  // next entry to finalise
+    for (uint32_t e = 0;; ++e) {
+      const bool issue = it_i < total;
+      if (issue) {
+        const int s = e % R;
+        if (lane == 0) {
           if (e >= R) tma::mbar_wait(&empty[s], ((e / R) - 1) & 1);
           tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
           double* dst = ring + s * kTmaSlot;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) tma::load_4d(dst + f * kTmaField, &map, a.g.off + ti0 - 2, tj0 - 2, pl, f, &full[s]);
+          for (int f = 0; f < 5; ++f)
+            tma::load_4d(dst + f * kTmaField, &map, a.g.off + gi.ti0 - 2, gi.tj0 - 2, pl_i, f, &full[s]);
         }
-        u += len;
+        if (++pl_i > gi.ke + 1) {
+          it_i += G;
+          if (it_i < total) {
+            gi = item_geom(a, it_i);
+            pl_i = gi.kb - 2;
+          }
+        }
+      }
+      if (e >= static_cast<uint32_t>(kTmaLag) || !issue) {
+        if (it_p >= total) break;
+        const int s = ep % R;
+        tma::mbar_wait(&full[s], (ep / R) & 1);
+        patch_plane(ring + s * kTmaSlot, a, gp, pl_p, pc, lane);
+        tma::fence_proxy_async();  // generic writes before the slot's next TMA fill
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(&ready[s]);
+        ++ep;
+        if (++pl_p > gp.ke + 1) {
+          it_p += G;
+          if (it_p < total) {
+            gp = item_geom(a, it_p);
+            pl_p = gp.kb - 2;
+          }
+        }
       }
     }
     return;
@@ -144,131 +307,70 @@ __global__ void __maxnreg__(112)
   // ---------------- consumers ----------------
   const int tx = lane, ty = warp;
   const Geo g = a.g;
-  const double pc = a.sc->pc, dt = a.sc->dt, u_ref = a.sp.u_ref;
+  const double dt = a.sc->dt, u_ref = a.sp.u_ref;
   const long long fs = g.fstride;
-  const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
-  const int kzh = g.nz + 2;
+  const bool zlo = a.walls.wall[4], zhi = a.walls.wall[5];
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
   unsigned bad = 0, nbad = 0;
   uint32_t e = 0;
-  const int cen = (ty + 2) * BW + tx + 2;  // own cell inside a field plane
+  const int cen = (ty + 2) * BW + tx + 2;
 
-  auto wait_full = [&](uint32_t idx) { tma::mbar_wait(&full[idx % R], (idx / R) & 1); };
+  auto wait_ready = [&](uint32_t idx) { tma::mbar_wait(&ready[idx % R], (idx / R) & 1); };
   auto release = [&](uint32_t idx) {
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&empty[idx % R]);
   };
-  auto fplane = [&](uint32_t idx, int f) -> const double* { return ring + (idx % R) * kTmaSlot + f * kTmaField; };
+  auto fp = [&](uint32_t idx, int f) -> const double* { return ring + (idx % R) * kTmaSlot + f * kTmaField + cen; };
 
-  for (long long u = u0; u < u1;) {
-    const int tile = static_cast<int>(u / bd);
-    const int kb = a.box.lo[2] + static_cast<int>(u % bd);
-    const long long rem_ = bd - u % bd;
-        const int len = static_cast<int>(rem_ < u1 - u ? rem_ : u1 - u);
-    const int ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
-    const int tj0 = a.box.lo[1] + (tile / a.tiles_x) * TY;
-    const int i = ti0 + tx, j = tj0 + ty;
+  for (long long item = blockIdx.x; item < total; item += G) {
+    const ItemGeom it = item_geom(a, item);
+    const int len = it.ke - it.kb;
+    const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
-    // in-plane pressure neighbours that are interior get the lazy shift
-    const bool sxm = i - 1 >= 2, sxm2 = i - 2 >= 2, sxp = i + 1 < g.nx + 2, sxp2 = i + 2 < g.nx + 2;
-    const bool sym = j - 1 >= 2, sym2 = j - 2 >= 2, syp = j + 1 < g.ny + 2, syp2 = j + 2 < g.ny + 2;
-    const bool all_in = sxm && sxm2 && sxp && sxp2 && sym && sym2 && syp && syp2;
-    auto pk = [&](double x, int k) { return x - (k >= 2 && k < kzh ? pc : 0.0); };
-
-    // prologue: planes kb-2 .. kb+1 (sequence e .. e+3)
-    wait_full(e);
-    wait_full(e + 1);
-    wait_full(e + 2);
-    wait_full(e + 3);
-    double pm2 = pk(fplane(e, 0)[cen], kb - 2);
-    double pm1 = pk(fplane(e + 1, 0)[cen], kb - 1);
-    double p0 = pk(fplane(e + 2, 0)[cen], kb);
-    double pp1 = pk(fplane(e + 3, 0)[cen], kb + 1);
-    double um1 = fplane(e + 1, 1)[cen], u0c = fplane(e + 2, 1)[cen];
-    double vm1 = fplane(e + 1, 2)[cen], v0c = fplane(e + 2, 2)[cen];
-    double wm1 = fplane(e + 1, 3)[cen], w0c = fplane(e + 2, 3)[cen];
-    double tm1 = fplane(e + 1, 4)[cen], t0c = fplane(e + 2, 4)[cen];
+    wait_ready(e);
+    wait_ready(e + 1);
+    wait_ready(e + 2);
+    wait_ready(e + 3);
+    double pm2 = *fp(e, 0), pm1 = *fp(e + 1, 0), p0 = *fp(e + 2, 0), pp1 = *fp(e + 3, 0);
+    double um1 = *fp(e + 1, 1), u0 = *fp(e + 2, 1);
+    double vm1 = *fp(e + 1, 2), v0 = *fp(e + 2, 2);
+    double wm1 = *fp(e + 1, 3), w0 = *fp(e + 2, 3);
+    double tm1 = *fp(e + 1, 4), t0 = *fp(e + 2, 4);
     release(e);
     release(e + 1);
-
     for (int s = 0; s < len; ++s) {
-      const int k = kb + s;
-      const uint32_t q = e + 2 + s;  // sequence index of plane k
-      wait_full(q + 2);
-      const double pp2 = pk(fplane(q + 2, 0)[cen], k + 2);
-      const double up1 = fplane(q + 1, 1)[cen], vp1 = fplane(q + 1, 2)[cen], wp1 = fplane(q + 1, 3)[cen],
-                   tp1 = fplane(q + 1, 4)[cen];
+      const int k = it.kb + s;
+      const uint32_t q = e + 2 + s;
+      wait_ready(q + 2);
+      double pp2 = *fp(q + 2, 0);
+      double up1 = *fp(q + 1, 1), vp1 = *fp(q + 1, 2), wp1 = *fp(q + 1, 3), tp1 = *fp(q + 1, 4);
+      // z-wall ghosts in the register window (uniform over the CTA)
+      if (zlo && k == 2) {
+        pm1 = cubic_g0(p0, pp1, pp2);
+        pm2 = cubic_g1(pm1, p0, pp1);
+        um1 = -u0;
+        vm1 = -v0;
+        wm1 = -w0;
+        tm1 = t0;
+      } else if (zlo && k == 3) {
+        pm2 = cubic_g0(pm1, p0, pp1);
+      }
+      if (zhi && k == g.nz) {
+        pp2 = cubic_g0(pp1, p0, pm1);
+      } else if (zhi && k == g.nz + 1) {
+        pp1 = cubic_g0(p0, pm1, pm2);
+        pp2 = cubic_g1(pp1, p0, pm1);
+        up1 = -u0;
+        vp1 = -v0;
+        wp1 = -w0;
+        tp1 = t0;
+      }
       if (active) {
-        const double* BP = fplane(q, 0) + cen;
-        Star st;
-        st.p = p0;
-        st.pxm = BP[-1];
-        st.pxp = BP[1];
-        st.pxm2 = BP[-2];
-        st.pxp2 = BP[2];
-        st.pym = BP[-BW];
-        st.pyp = BP[BW];
-        st.pym2 = BP[-2 * BW];
-        st.pyp2 = BP[2 * BW];
-        if (all_in) {
-          st.pxm -= pc;
-          st.pxp -= pc;
-          st.pxm2 -= pc;
-          st.pxp2 -= pc;
-          st.pym -= pc;
-          st.pyp -= pc;
-          st.pym2 -= pc;
-          st.pyp2 -= pc;
-        } else {
-          st.pxm -= sxm ? pc : 0.0;
-          st.pxp -= sxp ? pc : 0.0;
-          st.pxm2 -= sxm2 ? pc : 0.0;
-          st.pxp2 -= sxp2 ? pc : 0.0;
-          st.pym -= sym ? pc : 0.0;
-          st.pyp -= syp ? pc : 0.0;
-          st.pym2 -= sym2 ? pc : 0.0;
-          st.pyp2 -= syp2 ? pc : 0.0;
-        }
-        st.pzm = pm1;
-        st.pzp = pp1;
-        st.pzm2 = pm2;
-        st.pzp2 = pp2;
-        const double* BU = fplane(q, 1) + cen;
-        st.u = u0c;
-        st.uxm = BU[-1];
-        st.uxp = BU[1];
-        st.uym = BU[-BW];
-        st.uyp = BU[BW];
-        st.uzm = um1;
-        st.uzp = up1;
-        const double* BV = fplane(q, 2) + cen;
-        st.v = v0c;
-        st.vxm = BV[-1];
-        st.vxp = BV[1];
-        st.vym = BV[-BW];
-        st.vyp = BV[BW];
-        st.vzm = vm1;
-        st.vzp = vp1;
-        const double* BWp = fplane(q, 3) + cen;
-        st.w = w0c;
-        st.wxm = BWp[-1];
-        st.wxp = BWp[1];
-        st.wym = BWp[-BW];
-        st.wyp = BWp[BW];
-        st.wzm = wm1;
-        st.wzp = wp1;
-        const double* BT = fplane(q, 4) + cen;
-        st.t = t0c;
-        st.txm = BT[-1];
-        st.txp = BT[1];
-        st.tym = BT[-BW];
-        st.typ = BT[BW];
-        st.tzm = tm1;
-        st.tzp = tp1;
-        if (near_wall(a.walls, g, i, j, k)) apply_wall_ghosts(st, a.walls, g, i, j, k);
-        const Res r = residual_of(st, a.sp);
-        const double qp = p0 + dt * r.p, qu = u0c + dt * r.u, qv = v0c + dt * r.v, qw = w0c + dt * r.w,
-                     qt = t0c + dt * r.t;
+        const SmemAcc sa{fp(q, 0), fp(q, 1), fp(q, 2), fp(q, 3), fp(q, 4), p0,  pm1, pp1, pm2, pp2, u0, um1,
+                         up1,      v0,       vm1,      vp1,      w0,       wm1, wp1, t0,  tm1, tp1};
+        const Res r = residual_t(sa, a.sp);
+        const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
+                     qt = t0 + dt * r.t;
         const long long c = g.idx(i, j, k);
         a.out[c] = qp;
         a.out[fs + c] = qu;
@@ -291,28 +393,26 @@ __global__ void __maxnreg__(112)
           }
         }
       }
-      release(q);  // plane k is never read again
+      release(q);
       pm2 = pm1;
       pm1 = p0;
       p0 = pp1;
       pp1 = pp2;
-      um1 = u0c;
-      u0c = up1;
-      vm1 = v0c;
-      v0c = vp1;
-      wm1 = w0c;
-      w0c = wp1;
-      tm1 = t0c;
-      t0c = tp1;
+      um1 = u0;
+      u0 = up1;
+      vm1 = v0;
+      v0 = vp1;
+      wm1 = w0;
+      w0 = wp1;
+      tm1 = t0;
+      t0 = tp1;
     }
-    release(e + len + 2);  // planes ke, ke+1 served only as column values
+    release(e + len + 2);
     release(e + len + 3);
     e += len + 4;
-    u += len;
-    (void)plane;
   }
 
-  // consumer-only reductions (the producer warp has exited)
+  // consumer-only reductions
   constexpr int NC = 32 * C;
   __shared__ double sred[3][C];
   __shared__ unsigned smask[C];
@@ -329,7 +429,7 @@ __global__ void __maxnreg__(112)
     sred[2][warp] = m2;
     smask[warp] = bad | (nbad << 8);
   }
-  tma::consumer_sync(NC);
+  tma::named_sync(1, NC);
   if (threadIdx.x == 0) {
     unsigned mk = 0;
     for (int w = 0; w < C; ++w) {

@@ -5,6 +5,9 @@ import sys
 
 import pytest
 
+# before anything initialises CUDA: several test ranks share one GPU
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
