@@ -78,25 +78,36 @@ def test_oracle_error_paths_match_reference(golden, name):
     assert str(ex.value) == e["error"]
 
 
-def test_oracle_repro_sum_rounding():
-    """ReproSum exactness and round-to-nearest-even (tests/test_util.cpp:23-132)."""
+def test_oracle_repro_value_rounding():
+    """ReproSum::value rounding (inc/util/repro_sum.hpp:48-77), restated."""
     L = Oracle.lib()
 
-    def value_of(terms):
-        acc = np.zeros(70, dtype=np.uint64)
-        # accumulate via the norm-partials path: a 1-cell-per-term field trick is
-        # awkward, so restate through oc_norm_partials on squares
-        return acc
+    def val(limbs):
+        arr = np.ascontiguousarray(limbs, dtype=np.uint64)
+        return L.oc_repro_value(arr.ctypes.data_as(C.POINTER(C.c_uint64)))
 
-    big = 2.0 ** 53
-    # exact cancellation through limbs: build limbs by hand
     limbs = np.zeros(70, dtype=np.uint64)
-    limbs[0] = 1 << 3  # 8 * 2^-1140 -> subnormal-range, rounds via ldexp
-    assert L.oc_repro_value(limbs.ctypes.data_as(C.POINTER(C.c_uint64))) == np.ldexp(8.0, -1140)
+    limbs[0] = (1 << 53) + 1  # tie -> even
+    assert val(limbs) == np.ldexp(2.0 ** 53, -1140)
+    limbs[0] = (1 << 53) + 3  # tie, odd keep -> up
+    assert val(limbs) == np.ldexp(2.0 ** 53 + 4, -1140)
     limbs[:] = 0
     limbs[35] = 5  # negative half only
-    assert L.oc_repro_value(limbs.ctypes.data_as(C.POINTER(C.c_uint64))) == -np.ldexp(5.0, -1140)
-    del value_of, big
+    assert val(limbs) == -np.ldexp(5.0, -1140)
+
+
+@pytest.mark.skipif(not ref_available(), reason="reference library not built here")
+def test_oracle_norm_partials_equal_reference_limbs():
+    """Exact partials (serialised ReproSum limbs) equal the reference's."""
+    import oracle_ops as O
+    n = (9, 7, 6)
+    r = O.random_fields(n, 5)
+    r[2] *= 1e-158
+    want = np.zeros(350, dtype=np.uint64)
+    fp = A.FieldPtrs(*[r[v].ctypes.data for v in range(5)])
+    assert Ref.lib().ref_residual_norm_partials(C.byref(fp), n[0], n[1], n[2],
+                                                want.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+    np.testing.assert_array_equal(O.norm_limbs(r, n).ravel(), want)
 
 
 @pytest.mark.skipif(not ref_available(), reason="reference library not built here")
