@@ -776,6 +776,12 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   lay = arena_layout(plan, d.np);
 
   CAV_CUDA(cudaSetDevice(d.device));
+  {
+    int lo, hi;
+    CAV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CAV_CUDA(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, lo));
+    CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, hi));  // comm: high priority
+  }
   // padded layout: interior rows start 128-byte aligned (off 14 -> i=2 at 16)
   g.nx = n[0];
   g.ny = n[1];
@@ -786,7 +792,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   g.fstride = static_cast<long long>(align_up(static_cast<size_t>(g.pitch) * g.ypitch * (n[2] + 4), 32));
   for (int s = 0; s < 2; ++s) {
     CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
-    CAV_CUDA(cudaMemset(state[s], 0, 5 * g.fstride * sizeof(double)));
+    CAV_CUDA(cudaMemsetAsync(state[s], 0, 5 * g.fstride * sizeof(double), s0));
   }
   {  // load every kernel module now (see ops::preload_kernels)
     ops::preload_kernels();
@@ -820,26 +826,26 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     tma_grid = std::max(1, per_sm) * sms;
   }
   CAV_CUDA(cudaMalloc(&arena, lay.bytes));
-  CAV_CUDA(cudaMemset(arena, 0, lay.bytes));
+  // Stream-ordered and completed before any peer can see this arena: a
+  // legacy-stream cudaMemset is not ordered against the non-blocking streams
+  // of other ranks and could wipe a flag a fast peer already wrote.
+  CAV_CUDA(cudaMemsetAsync(arena, 0, lay.bytes, s0));
   CAV_CUDA(cudaMalloc(&acc, 2 * sizeof(Acc)));
   CAV_CUDA(cudaMalloc(&sc, 2 * sizeof(IterScalars)));
   CAV_CUDA(cudaMalloc(&err, 2 * sizeof(unsigned long long)));
   tflag = err + 1;
   CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
-  CAV_CUDA(cudaMemset(counters, 0, 64 * sizeof(unsigned)));
+  CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
   if (!plan.empty()) {
     CAV_CUDA(cudaMalloc(&d_pack, plan.size() * sizeof(MsgDesc)));
     CAV_CUDA(cudaMalloc(&d_unpack, plan.size() * sizeof(MsgDesc)));
   }
-  int lo, hi;
-  CAV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  CAV_CUDA(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, lo));
-  CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, hi));  // comm: high priority
   CAV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   CAV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   ev_a = make_event();
   ev_b = make_event();
+  CAV_CUDA(cudaStreamSynchronize(s0));
   peer_arena.assign(d.np, nullptr);
   peer_ipc.assign(d.np, false);
   peer_arena[d.rank] = arena;
@@ -1250,8 +1256,9 @@ int cav_block_upload(cav_block* bh, const double* host5) {
     const size_t X = b.n[0] + 4, Y = b.n[1] + 4, Z = b.n[2] + 4;
     for (int s = 0; s < 2; ++s)
       for (int v = 0; v < 5; ++v)
-        CAV_CUDA(cudaMemcpy2D(b.field(s, v) + b.g.off, b.g.pitch * sizeof(double), host5 + v * X * Y * Z,
-                              X * sizeof(double), X * sizeof(double), Y * Z, cudaMemcpyHostToDevice));
+        CAV_CUDA(cudaMemcpy2DAsync(b.field(s, v) + b.g.off, b.g.pitch * sizeof(double), host5 + v * X * Y * Z,
+                                   X * sizeof(double), X * sizeof(double), Y * Z, cudaMemcpyHostToDevice, b.s0));
+    CAV_CUDA(cudaStreamSynchronize(b.s0));  // ordered with this block's non-blocking streams
     b.cur = 0;
     b.next_n = 1;
     b.primed = false;

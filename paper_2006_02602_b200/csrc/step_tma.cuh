@@ -1,13 +1,14 @@
 // step_tma.cuh — the fused pseudo-time step (K4), TMA-fed and warp-specialised.
 //
-// One persistent CTA per SM: 1 producer warp + TY consumer warps (a 32 x TY
-// tile of cells per plane, one cell per consumer thread).
+// One persistent CTA per SM: TY consumer warps (a 32 x TY tile of cells per
+// plane, one cell per consumer thread), one TMA issuer warp, one patcher warp.
 //
-// Producer warp: streams 36 x (TY+4) plane tiles of all five fields (tile plus
-// a 2-cell halo ring) into a ring of R shared-memory slots with
-// cp.async.bulk.tensor.4d (completion = mbarrier transaction count). LAG
-// entries behind the issue front it finalises each landed plane in place —
-// the lazy rescale fl(p - pc) on interior pressure, and the wall ghosts of
+// Issuer (one lane): streams 36 x (TY+4) plane tiles of all five fields (tile
+// plus a 2-cell halo ring) into a ring of R shared-memory slots with
+// cp.async.bulk.tensor.4d (completion = the slot's `full` mbarrier transaction
+// count); it only waits for a slot to be released (`empty`).
+// Patcher (whole warp): as each plane lands it finalises it in place — the
+// lazy rescale fl(p - pc) on interior pressure, and the wall ghosts of
 // apply_boundary_conditions (src/solver.cpp:158-191) for x/y walls — and
 // arrives on the slot's `ready` mbarrier. So consumers read final values only.
 //
@@ -74,15 +75,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 constexpr int kTmaTY = 16;                              // consumer warps = tile rows
 constexpr int kTmaRing = 7;                             // plane slots
-constexpr int kTmaLag = 3;                              // patch lag behind the TMA front
 constexpr int kTmaBW = 36;                              // 32 + 2x2 halo
 constexpr int kTmaBH = kTmaTY + 4;
 constexpr int kTmaField = kTmaBW * kTmaBH;              // doubles per field plane
 constexpr int kTmaSlot = 5 * kTmaField;                 // doubles per slot
-constexpr int kTmaThreads = 32 * (kTmaTY + 1);
+constexpr int kTmaThreads = 32 * (kTmaTY + 2);         // consumers + issuer + patcher
 constexpr size_t kTmaSmem = kTmaRing * kTmaSlot * sizeof(double) + 3 * kTmaRing * 8 + 5 * kDigits * 8;
 static_assert(kTmaField * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
-static_assert(kTmaRing >= kTmaLag + 4, "ring too small for the patch lag (deadlock)");
+static_assert(kTmaRing >= 5, "ring must hold planes k..k+2 plus prefetch");
 
 struct TmaStepArgs {
   double* out;
@@ -155,11 +155,27 @@ __device__ __forceinline__ void patch_plane(double* slot, const TmaStepArgs& a, 
   if (pl < 2 || pl >= g.nz + 2) return;  // ghost planes: read only as column values
   double* P = slot;
   const int i0 = it.ti0 - 2, j0 = it.tj0 - 2;
-  // lazy rescale of interior pressure (rescale_pressure, src/solver.cpp:248-257)
-  for (int e = lane; e < kTmaField; e += 32) {
-    const int x = e % kTmaBW, y = e / kTmaBW;
-    const int i = i0 + x, j = j0 + y;
-    if (i >= 2 && i < g.nx + 2 && j >= 2 && j < g.ny + 2) P[e] = P[e] - pc;
+  // lazy rescale of interior pressure (rescale_pressure, src/solver.cpp:248-257),
+  // two doubles per lane access; element (x, y) is cell (i0 + x, j0 + y)
+  {
+    constexpr int PAIRS = kTmaBW / 2;
+    int row = lane / PAIRS, c = lane % PAIRS;
+    for (int idx = lane; idx < kTmaBH * PAIRS; idx += 32) {
+      const int j = j0 + row, i = i0 + 2 * c;
+      if (j >= 2 && j < g.ny + 2) {
+        double2* q = reinterpret_cast<double2*>(P + row * kTmaBW + 2 * c);
+        double2 v = *q;
+        if (i >= 2 && i < g.nx + 2) v.x = v.x - pc;
+        if (i + 1 >= 2 && i + 1 < g.nx + 2) v.y = v.y - pc;
+        *q = v;
+      }
+      c += 32 - PAIRS;  // idx += 32 in (row, c) coordinates
+      row += 1;
+      if (c >= PAIRS) {
+        c -= PAIRS;
+        row += 1;
+      }
+    }
   }
   __syncwarp();
   const WallInfo& w = a.walls;
@@ -256,48 +272,42 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const double pc = a.sc->pc;
 
   if (warp == C) {
-    // ---------------- producer ----------------
-    long long it_i = blockIdx.x, it_p = blockIdx.x;  // issue / patch cursors (items)
-    ItemGeom gi{0, 0, 0, 0};
-    if (it_i < total) gi = item_geom(a, it_i);
-    ItemGeom gp = gi;
-    int pl_i = gi.kb - 2, pl_p = gi.kb - 2;
-    uint32_t ep = 0;  // next entry to finalise
-    for (uint32_t e = 0;; ++e) {
-      const bool issue = it_i < total;
-      if (issue) {
-        const int s = e % R;
-        if (lane == 0) {
-          if (e >= R) tma::mbar_wait(&empty[s], ((e / R) - 1) & 1);
-          tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
-          double* dst = ring + s * kTmaSlot;
+    // ---------------- TMA issuer (one lane) ----------------
+    if (lane != 0) return;
+    int s = 0;
+    uint32_t ph = 0, e = 0;  // slot / empty-barrier phase of entry e
+    for (long long item = blockIdx.x; item < total; item += G) {
+      const ItemGeom it = item_geom(a, item);
+      const int x0 = a.g.off + it.ti0 - 2, y0 = it.tj0 - 2;
+      for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl, ++e) {
+        if (e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[s], ph ^ 1);
+        tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
+        double* dst = ring + s * kTmaSlot;
 #pragma unroll
-          for (int f = 0; f < 5; ++f)
-            tma::load_4d(dst + f * kTmaField, &map, a.g.off + gi.ti0 - 2, gi.tj0 - 2, pl_i, f, &full[s]);
-        }
-        if (++pl_i > gi.ke + 1) {
-          it_i += G;
-          if (it_i < total) {
-            gi = item_geom(a, it_i);
-            pl_i = gi.kb - 2;
-          }
+        for (int f = 0; f < 5; ++f) tma::load_4d(dst + f * kTmaField, &map, x0, y0, pl, f, &full[s]);
+        if (++s == R) {
+          s = 0;
+          ph ^= 1;
         }
       }
-      if (e >= static_cast<uint32_t>(kTmaLag) || !issue) {
-        if (it_p >= total) break;
-        const int s = ep % R;
-        tma::mbar_wait(&full[s], (ep / R) & 1);
-        patch_plane(ring + s * kTmaSlot, a, gp, pl_p, pc, lane);
+    }
+    return;
+  }
+  if (warp == C + 1) {
+    // ---------------- patcher (whole warp) ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long item = blockIdx.x; item < total; item += G) {
+      const ItemGeom it = item_geom(a, item);
+      for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl) {
+        tma::mbar_wait(&full[s], ph);
+        patch_plane(ring + s * kTmaSlot, a, it, pl, pc, lane);
         tma::fence_proxy_async();  // generic writes before the slot's next TMA fill
         __syncwarp();
         if (lane == 0) tma::mbar_arrive(&ready[s]);
-        ++ep;
-        if (++pl_p > gp.ke + 1) {
-          it_p += G;
-          if (it_p < total) {
-            gp = item_geom(a, it_p);
-            pl_p = gp.kb - 2;
-          }
+        if (++s == R) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
@@ -309,81 +319,112 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const Geo g = a.g;
   const double dt = a.sc->dt, u_ref = a.sp.u_ref;
   const long long fs = g.fstride;
+  const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
   const bool zlo = a.walls.wall[4], zhi = a.walls.wall[5];
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-  unsigned bad = 0, nbad = 0;
-  uint32_t e = 0;
-  const int cen = (ty + 2) * BW + tx + 2;
-
-  auto wait_ready = [&](uint32_t idx) { tma::mbar_wait(&ready[idx % R], (idx / R) & 1); };
-  auto release = [&](uint32_t idx) {
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[idx % R]);
+  unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
+  unsigned nbad = 0;
+  const double* ringc = ring + (ty + 2) * BW + tx + 2;  // own cell in slot 0, field 0
+  // rolling ring cursor: slot of the next entry to wait for, and its phase
+  int sw = 0;
+  uint32_t phw = 0;
+  auto advance = [&](int& sl, uint32_t& ph) {
+    if (++sl == R) {
+      sl = 0;
+      ph ^= 1;
+    }
   };
-  auto fp = [&](uint32_t idx, int f) -> const double* { return ring + (idx % R) * kTmaSlot + f * kTmaField + cen; };
+  auto release_slot = [&](int sl) {
+    __syncwarp();
+    if (lane == 0) tma::mbar_arrive(&empty[sl]);
+  };
 
   for (long long item = blockIdx.x; item < total; item += G) {
     const ItemGeom it = item_geom(a, item);
     const int len = it.ke - it.kb;
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
-    wait_ready(e);
-    wait_ready(e + 1);
-    wait_ready(e + 2);
-    wait_ready(e + 3);
-    double pm2 = *fp(e, 0), pm1 = *fp(e + 1, 0), p0 = *fp(e + 2, 0), pp1 = *fp(e + 3, 0);
-    double um1 = *fp(e + 1, 1), u0 = *fp(e + 2, 1);
-    double vm1 = *fp(e + 1, 2), v0 = *fp(e + 2, 2);
-    double wm1 = *fp(e + 1, 3), w0 = *fp(e + 2, 3);
-    double tm1 = *fp(e + 1, 4), t0 = *fp(e + 2, 4);
-    release(e);
-    release(e + 1);
-    for (int s = 0; s < len; ++s) {
-      const int k = it.kb + s;
-      const uint32_t q = e + 2 + s;
-      wait_ready(q + 2);
-      double pp2 = *fp(q + 2, 0);
-      double up1 = *fp(q + 1, 1), vp1 = *fp(q + 1, 2), wp1 = *fp(q + 1, 3), tp1 = *fp(q + 1, 4);
+    const bool ccol = i == a.cx && j == a.cy;
+    // prologue: entries for planes kb-2, kb-1, kb, kb+1
+    int s0 = sw;
+    tma::mbar_wait(&ready[sw], phw);
+    advance(sw, phw);
+    int s1 = sw;
+    tma::mbar_wait(&ready[sw], phw);
+    advance(sw, phw);
+    int s2 = sw;
+    tma::mbar_wait(&ready[sw], phw);
+    advance(sw, phw);
+    int s3 = sw;
+    tma::mbar_wait(&ready[sw], phw);
+    advance(sw, phw);
+    const double* B0 = ringc + s0 * kTmaSlot;
+    const double* B1 = ringc + s1 * kTmaSlot;
+    const double* B2 = ringc + s2 * kTmaSlot;
+    const double* B3 = ringc + s3 * kTmaSlot;
+    double pm2 = B0[0], pm1 = B1[0], p0 = B2[0], pp1 = B3[0];
+    double um1 = B1[kTmaField], u0 = B2[kTmaField];
+    double vm1 = B1[2 * kTmaField], v0 = B2[2 * kTmaField];
+    double wm1 = B1[3 * kTmaField], w0 = B2[3 * kTmaField];
+    double tm1 = B1[4 * kTmaField], t0 = B2[4 * kTmaField];
+    release_slot(s0);
+    release_slot(s1);
+    // slots of planes k (cur) and k+1 (nxt); sw/phw = slot of plane k+2
+    int scur = s2, snxt = s3;
+    double* op = a.out + g.idx(i, j, it.kb);
+    for (int st = 0; st < len; ++st, op += plane) {
+      const int k = it.kb + st;
+      const int sk2 = sw;
+      tma::mbar_wait(&ready[sw], phw);
+      advance(sw, phw);
+      const double* Bc = ringc + scur * kTmaSlot;
+      const double* Bn = ringc + snxt * kTmaSlot;
+      double pp2 = (ringc + sk2 * kTmaSlot)[0];
+      double up1 = Bn[kTmaField], vp1 = Bn[2 * kTmaField], wp1 = Bn[3 * kTmaField], tp1 = Bn[4 * kTmaField];
       // z-wall ghosts in the register window (uniform over the CTA)
-      if (zlo && k == 2) {
-        pm1 = cubic_g0(p0, pp1, pp2);
-        pm2 = cubic_g1(pm1, p0, pp1);
-        um1 = -u0;
-        vm1 = -v0;
-        wm1 = -w0;
-        tm1 = t0;
-      } else if (zlo && k == 3) {
-        pm2 = cubic_g0(pm1, p0, pp1);
-      }
-      if (zhi && k == g.nz) {
-        pp2 = cubic_g0(pp1, p0, pm1);
-      } else if (zhi && k == g.nz + 1) {
-        pp1 = cubic_g0(p0, pm1, pm2);
-        pp2 = cubic_g1(pp1, p0, pm1);
-        up1 = -u0;
-        vp1 = -v0;
-        wp1 = -w0;
-        tp1 = t0;
+      if ((zlo && k <= 3) || (zhi && k >= g.nz)) {
+        if (zlo && k == 2) {
+          pm1 = cubic_g0(p0, pp1, pp2);
+          pm2 = cubic_g1(pm1, p0, pp1);
+          um1 = -u0;
+          vm1 = -v0;
+          wm1 = -w0;
+          tm1 = t0;
+        } else if (zlo && k == 3) {
+          pm2 = cubic_g0(pm1, p0, pp1);
+        }
+        if (zhi && k == g.nz) {
+          pp2 = cubic_g0(pp1, p0, pm1);
+        } else if (zhi && k == g.nz + 1) {
+          pp1 = cubic_g0(p0, pm1, pm2);
+          pp2 = cubic_g1(pp1, p0, pm1);
+          up1 = -u0;
+          vp1 = -v0;
+          wp1 = -w0;
+          tp1 = t0;
+        }
       }
       if (active) {
-        const SmemAcc sa{fp(q, 0), fp(q, 1), fp(q, 2), fp(q, 3), fp(q, 4), p0,  pm1, pp1, pm2, pp2, u0, um1,
-                         up1,      v0,       vm1,      vp1,      w0,       wm1, wp1, t0,  tm1, tp1};
+        const SmemAcc sa{Bc, Bc + kTmaField, Bc + 2 * kTmaField, Bc + 3 * kTmaField, Bc + 4 * kTmaField,
+                         p0, pm1, pp1, pm2, pp2, u0, um1, up1, v0, vm1, vp1, w0, wm1, wp1, t0, tm1, tp1};
         const Res r = residual_t(sa, a.sp);
         const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
                      qt = t0 + dt * r.t;
-        const long long c = g.idx(i, j, k);
-        a.out[c] = qp;
-        a.out[fs + c] = qu;
-        a.out[2 * fs + c] = qv;
-        a.out[3 * fs + c] = qw;
-        a.out[4 * fs + c] = qt;
+        op[0] = qp;
+        op[fs] = qu;
+        op[2 * fs] = qv;
+        op[3 * fs] = qw;
+        op[4 * fs] = qt;
         const Denoms d = cfl_denoms(qu, qv, qw, u_ref);
         m0 = dmax_d(m0, d.du);
         m1 = dmax_d(m1, d.dv);
         m2 = dmax_d(m2, d.dw);
-        bad |= nonfinite(qp) | (nonfinite(qu) << 1) | (nonfinite(qv) << 2) | (nonfinite(qw) << 3) |
-               (nonfinite(qt) << 4);
-        if (i == a.cx && j == a.cy && k == a.cz) a.acc->pc_local = qp;
+        e_p = max(e_p, static_cast<unsigned>(__double2hiint(qp)) & 0x7FF00000u);
+        e_u = max(e_u, static_cast<unsigned>(__double2hiint(qu)) & 0x7FF00000u);
+        e_v = max(e_v, static_cast<unsigned>(__double2hiint(qv)) & 0x7FF00000u);
+        e_w = max(e_w, static_cast<unsigned>(__double2hiint(qw)) & 0x7FF00000u);
+        e_t = max(e_t, static_cast<unsigned>(__double2hiint(qt)) & 0x7FF00000u);
+        if (ccol && k == a.cz) a.acc->pc_local = qp;
         if (NORMS) {
           const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
 #pragma unroll
@@ -393,7 +434,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           }
         }
       }
-      release(q);
+      release_slot(scur);
+      scur = snxt;
+      snxt = sk2;
       pm2 = pm1;
       pm1 = p0;
       p0 = pp1;
@@ -407,10 +450,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       tm1 = t0;
       t0 = tp1;
     }
-    release(e + len + 2);
-    release(e + len + 3);
-    e += len + 4;
+    release_slot(scur);  // planes ke, ke+1 served only as column values
+    release_slot(snxt);
   }
+  constexpr unsigned EXP = 0x7FF00000u;
+  unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
+                 (e_w == EXP ? 8u : 0u) | (e_t == EXP ? 16u : 0u);
 
   // consumer-only reductions
   constexpr int NC = 32 * C;
