@@ -404,7 +404,15 @@ struct MsgDesc {
   int peer;
 };
 
+// Progress stamps (diagnostics): stage -> last iteration that reached it.
+enum DbgStage { kDbgPackStart, kDbgPackFlag, kDbgWaitStart, kDbgWaitDone, kDbgUnpackDone, kDbgSyncPush,
+                kDbgSyncDone, kDbgStages };
+__device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int stage, long long n) {
+  if (dbg) atomicMax(dbg + stage, static_cast<unsigned long long>(n));
+}
+
 struct XArgs {
+  unsigned long long* dbg;
   double* state;
   Geo g;
   const MsgDesc* msg;
@@ -431,6 +439,7 @@ __device__ __forceinline__ void msg_locate(const MsgDesc& m, long long q, int& v
 }
 
 __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg_stamp(a.dbg, kDbgPackStart, a.n);
   const MsgDesc& m = a.msg[blockIdx.y];
   const double pc = a.sc->pc;
   double* dst = m.slab + (a.n & 1) * m.scalars;
@@ -454,6 +463,7 @@ __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
       *m.counter = 0;
       __threadfence_system();
       st_release_sys(m.flag, static_cast<unsigned long long>(a.n));
+      dbg_stamp(a.dbg, kDbgPackFlag, a.n);
     }
   }
 }
@@ -463,6 +473,7 @@ __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
 // share one GPU (the in-process test topology).
 __global__ void __launch_bounds__(32) k_wait_flags(const XArgs a, int nmsg) {
   if (*reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull) return;  // already failed
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgWaitStart, a.n);
   for (int m = threadIdx.x; m < nmsg; m += 32) {
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(a.msg[m].flag) < static_cast<unsigned long long>(a.n)) {
@@ -474,6 +485,7 @@ __global__ void __launch_bounds__(32) k_wait_flags(const XArgs a, int nmsg) {
     }
   }
   __threadfence();
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgWaitDone, a.n);
 }
 
 __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
@@ -507,6 +519,7 @@ struct Slot {
 static_assert(sizeof(Slot) == 64, "slot size");
 
 struct SyncArgs {
+  unsigned long long* dbg;
   Acc* acc_cur;
   Acc* acc_next;
   IterScalars* sc_next;
@@ -544,6 +557,7 @@ __global__ void __launch_bounds__(kSyncThreads) k_scalar_sync(const SyncArgs a) 
   }
   unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
   __syncthreads();
+  if (tid == 0) dbg_stamp(a.dbg, kDbgSyncPush, a.n);
   const bool failed = *reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull;
   for (int r = tid; r < a.np; r += kSyncThreads) {
     const Slot* s = a.my_slots + (r * 2 + par);
@@ -580,6 +594,7 @@ __global__ void __launch_bounds__(kSyncThreads) k_scalar_sync(const SyncArgs a) 
     Acc z{};
     z.err = ~0ull;
     *a.acc_next = z;
+    dbg_stamp(a.dbg, kDbgSyncDone, a.n);
   }
 }
 
@@ -714,6 +729,7 @@ struct Block {
   IterScalars* sc = nullptr;     // [2]
   unsigned long long* err = nullptr;      // sticky min error code
   unsigned long long* tflag = nullptr;    // timeout code
+  unsigned long long* dbg = nullptr;      // progress stamps
   unsigned* counters = nullptr;
   MsgDesc* d_pack = nullptr;
   MsgDesc* d_unpack = nullptr;
@@ -834,6 +850,8 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaMalloc(&sc, 2 * sizeof(IterScalars)));
   CAV_CUDA(cudaMalloc(&err, 2 * sizeof(unsigned long long)));
   tflag = err + 1;
+  CAV_CUDA(cudaMalloc(&dbg, kDbgStages * sizeof(unsigned long long)));
+  CAV_CUDA(cudaMemsetAsync(dbg, 0, kDbgStages * sizeof(unsigned long long), s0));
   CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
@@ -865,6 +883,7 @@ Block::~Block() {
   cudaFree(sc);
   cudaFree(err);
   cudaFree(counters);
+  cudaFree(dbg);
   cudaFree(d_peer_slots);
   cudaFree(d_pack);
   cudaFree(d_unpack);
@@ -944,6 +963,7 @@ void Block::prologue() {
   const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
   ops::launch_dt_scan(f, g, ib, sp.u_ref, acc, 1, d.rank, s0);  // dt_1 from the initial state
   SyncArgs a{};
+  a.dbg = dbg;
   a.acc_cur = acc;
   a.acc_next = acc + 1;
   a.sc_next = sc + 1;
@@ -1065,6 +1085,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
   double* f[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
   if (!use_tma) ops::launch_bc(f, g, walls, d.fluid, sc_n, s0);  // v1 kernel reads stored wall ghosts
   XArgs x{};
+  x.dbg = dbg;
   x.state = state[cur];
   x.g = g;
   x.n = it;
@@ -1121,6 +1142,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
     launch_shells(it, check, dig);
   }
   SyncArgs a{};
+  a.dbg = dbg;
   a.acc_cur = acc + (it & 1);
   a.acc_next = acc + ((it + 1) & 1);
   a.sc_next = sc + ((it + 1) & 1);
@@ -1391,12 +1413,13 @@ int cav_block_debug(cav_block* bh, uint64_t* out, int cap) {
     CAV_CUDA(cudaSetDevice(b.d.device));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s1));
-    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64);
+    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64 + kDbgStages);
     CAV_CUDA(cudaMemcpy(v.data(), b.arena, (64 + 16 * b.d.np) * 8, cudaMemcpyDeviceToHost));
     CAV_CUDA(cudaMemcpy(v.data() + 64 + 16 * b.d.np, b.err, 16, cudaMemcpyDeviceToHost));
     std::vector<unsigned> c(64);
     CAV_CUDA(cudaMemcpy(c.data(), b.counters, 64 * 4, cudaMemcpyDeviceToHost));
     for (int q = 0; q < 64; ++q) v[66 + 16 * b.d.np + q] = c[q];
+    CAV_CUDA(cudaMemcpy(v.data() + 130 + 16 * b.d.np, b.dbg, kDbgStages * 8, cudaMemcpyDeviceToHost));
     for (size_t q = 0; q < v.size() && static_cast<int>(q) < cap; ++q) out[q] = v[q];
   });
 }
