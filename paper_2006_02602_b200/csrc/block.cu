@@ -687,14 +687,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 4-D view (x = padded row, y, z, field) of one 5-field state for TMA; box =
 // one 36 x (TY+4) plane tile of one field.
-CUtensorMap make_state_map(const double* base, const Geo& g) {
+CUtensorMap make_state_map(const double* base, const Geo& g, int bh) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(g.ypitch),
                               static_cast<cuuint64_t>(g.nz + 4), 5};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.pitch) * 8,
                                  static_cast<cuuint64_t>(g.pitch) * g.ypitch * 8,
                                  static_cast<cuuint64_t>(g.fstride) * 8};
-  const cuuint32_t box[4] = {kTmaBW, kTmaBH, 1, 1};
+  const cuuint32_t box[4] = {kTmaBW, static_cast<cuuint32_t>(bh), 1, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -702,6 +702,39 @@ CUtensorMap make_state_map(const double* base, const Geo& g) {
                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return m;
+}
+
+// TMA step variants (tile height, ring depth, CTAs per SM); CAV_TMA_CFG picks
+// one for experiments, variant 0 is the default.
+using TmaV0 = TmaCfg<16, 7, 1>;
+using TmaV1 = TmaCfg<8, 6, 2>;
+using TmaV2 = TmaCfg<8, 12, 1>;
+using TmaV3 = TmaCfg<12, 9, 1>;
+constexpr int kTmaVariants = 4;
+constexpr int kTmaVariantTY[kTmaVariants] = {TmaV0::TY, TmaV1::TY, TmaV2::TY, TmaV3::TY};
+
+template <class Cfg>
+int tma_setup(int device) {
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::Smem)));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::Smem)));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  cudaFuncAttributes fa;
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, false>));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, true>));
+  int per_sm = 0, sms = 0;
+  CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<Cfg, false>, Cfg::Threads, Cfg::Smem));
+  CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  return std::max(1, std::min(per_sm, Cfg::CTAS)) * sms;
+}
+
+template <class Cfg>
+void tma_launch(const CUtensorMap& m, const TmaStepArgs& a, bool check, int grid, cudaStream_t st) {
+  if (check) k_step_tma<Cfg, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m, a);
+  else k_step_tma<Cfg, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m, a);
+  CAV_CUDA(cudaGetLastError());
 }
 
 struct Block {
@@ -747,6 +780,7 @@ struct Block {
   CUtensorMap tmap[2];
   WallInfo winfo{};
   int tma_grid = 0;
+  int tma_variant = 0;
   bool use_tma = true;
 
   explicit Block(const cav_block_desc& desc);
@@ -793,10 +827,14 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
 
   CAV_CUDA(cudaSetDevice(d.device));
   {
+    // The comm stream may run at high priority (CAV_COMM_PRIORITY=1) so its
+    // small kernels win CTA slots; default is equal priority.
     int lo, hi;
     CAV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* pr = std::getenv("CAV_COMM_PRIORITY");
+    const bool high = pr && std::atoi(pr) != 0;
     CAV_CUDA(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, lo));
-    CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, hi));  // comm: high priority
+    CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, high ? hi : lo));
   }
   // padded layout: interior rows start 128-byte aligned (off 14 -> i=2 at 16)
   g.nx = n[0];
@@ -815,8 +853,6 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     cudaFuncAttributes fa;
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, false>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, true>));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<false>));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<true>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<false>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<true>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_pack));
@@ -826,20 +862,18 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
   }
-  for (int s = 0; s < 2; ++s) tmap[s] = make_state_map(state[s], g);
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");
     use_tma = !(k && std::string(k) == "tiled");
-    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kTmaSmem)));
-    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kTmaSmem)));
-    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CAV_CUDA(cudaFuncSetAttribute(k_step_tma<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    int per_sm = 0, sms = 0;
-    CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<false>, kTmaThreads, kTmaSmem));
-    CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
-    tma_grid = std::max(1, per_sm) * sms;
+    const char* v = std::getenv("CAV_TMA_CFG");
+    tma_variant = v ? std::max(0, std::min(kTmaVariants - 1, std::atoi(v))) : 0;
+    switch (tma_variant) {
+      case 1: tma_grid = tma_setup<TmaV1>(d.device); break;
+      case 2: tma_grid = tma_setup<TmaV2>(d.device); break;
+      case 3: tma_grid = tma_setup<TmaV3>(d.device); break;
+      default: tma_grid = tma_setup<TmaV0>(d.device); break;
+    }
+    for (int s = 0; s < 2; ++s) tmap[s] = make_state_map(state[s], g, kTmaVariantTY[tma_variant] + 4);
   }
   CAV_CUDA(cudaMalloc(&arena, lay.bytes));
   // Stream-ordered and completed before any peer can see this arena: a
@@ -1006,7 +1040,8 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.rank = d.rank;
     const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
     a.tiles_x = (bw + 31) / 32;
-    a.ntiles = a.tiles_x * ((bh + kTmaTY - 1) / kTmaTY);
+    const int ty = kTmaVariantTY[tma_variant];
+    a.ntiles = a.tiles_x * ((bh + ty - 1) / ty);
     // k-chunk: balance items over the persistent grid (rounds/ceil(rounds))
     // while keeping the per-item window restart (4 extra planes) small
     double best = -1.0;
@@ -1024,9 +1059,12 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.walls = winfo;
     const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
     const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
-    if (check) k_step_tma<true><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
-    else k_step_tma<false><<<grid, kTmaThreads, kTmaSmem, s0>>>(tmap[cur], a);
-    CAV_CUDA(cudaGetLastError());
+    switch (tma_variant) {
+      case 1: tma_launch<TmaV1>(tmap[cur], a, check, grid, s0); break;
+      case 2: tma_launch<TmaV2>(tmap[cur], a, check, grid, s0); break;
+      case 3: tma_launch<TmaV3>(tmap[cur], a, check, grid, s0); break;
+      default: tma_launch<TmaV0>(tmap[cur], a, check, grid, s0); break;
+    }
     return;
   }
   StepArgs a{};

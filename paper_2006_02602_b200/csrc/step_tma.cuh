@@ -73,16 +73,20 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 }  // namespace tma
 
-constexpr int kTmaTY = 16;                              // consumer warps = tile rows
-constexpr int kTmaRing = 7;                             // plane slots
-constexpr int kTmaBW = 36;                              // 32 + 2x2 halo
-constexpr int kTmaBH = kTmaTY + 4;
-constexpr int kTmaField = kTmaBW * kTmaBH;              // doubles per field plane
-constexpr int kTmaSlot = 5 * kTmaField;                 // doubles per slot
-constexpr int kTmaThreads = 32 * (kTmaTY + 2);         // consumers + issuer + patcher
-constexpr size_t kTmaSmem = kTmaRing * kTmaSlot * sizeof(double) + 3 * kTmaRing * 8 + 5 * kDigits * 8;
-static_assert(kTmaField * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
-static_assert(kTmaRing >= 5, "ring must hold planes k..k+2 plus prefetch");
+constexpr int kTmaBW = 36;  // 32 + 2x2 halo
+
+// Tile height TY (= consumer warps), ring depth R and CTAs per SM.
+template <int TY_, int R_, int CTAS_>
+struct TmaCfg {
+  static constexpr int TY = TY_, R = R_, CTAS = CTAS_;
+  static constexpr int BH = TY + 4;
+  static constexpr int Field = kTmaBW * BH;  // doubles per field plane
+  static constexpr int Slot = 5 * Field;     // doubles per slot
+  static constexpr int Threads = 32 * (TY + 2);  // consumers + issuer + patcher
+  static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + 5 * kDigits * 8;
+  static_assert(Field * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
+  static_assert(R >= 5, "ring must hold planes k..k+2 plus prefetch");
+};
 
 struct TmaStepArgs {
   double* out;
@@ -103,12 +107,13 @@ struct ItemGeom {
   int ti0, tj0, kb, ke;
 };
 
+template <int TY>
 __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long item) {
   const int chunk = static_cast<int>(item / a.ntiles);
   const int tile = static_cast<int>(item % a.ntiles);
   ItemGeom r;
   r.ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
-  r.tj0 = a.box.lo[1] + (tile / a.tiles_x) * kTmaTY;
+  r.tj0 = a.box.lo[1] + (tile / a.tiles_x) * TY;
   r.kb = a.box.lo[2] + chunk * a.chunk;
   r.ke = min(r.kb + a.chunk, a.box.hi[2]);
   return r;
@@ -149,8 +154,10 @@ struct SmemAcc {
 };
 
 // Producer: finalise one landed plane tile in shared memory (all 32 lanes).
+template <int BH>
 __device__ __forceinline__ void patch_plane(double* slot, const TmaStepArgs& a, const ItemGeom& it, int pl,
                                             double pc, int lane) {
+  constexpr int kTmaBH = BH, kTmaField = kTmaBW * BH;
   const Geo& g = a.g;
   if (pl < 2 || pl >= g.nz + 2) return;  // ghost planes: read only as column values
   double* P = slot;
@@ -243,10 +250,11 @@ __device__ __forceinline__ void patch_plane(double* slot, const TmaStepArgs& a, 
   }
 }
 
-template <bool NORMS>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <class Cfg, bool NORMS>
+__global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     k_step_tma(const __grid_constant__ CUtensorMap map, const TmaStepArgs a) {
-  constexpr int C = kTmaTY, R = kTmaRing, BW = kTmaBW;
+  constexpr int C = Cfg::TY, R = Cfg::R, BW = kTmaBW;
+  constexpr int kTmaField = Cfg::Field, kTmaSlot = Cfg::Slot, kTmaThreads = Cfg::Threads;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + R * kTmaSlot * sizeof(double));
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     int s = 0;
     uint32_t ph = 0, e = 0;  // slot / empty-barrier phase of entry e
     for (long long item = blockIdx.x; item < total; item += G) {
-      const ItemGeom it = item_geom(a, item);
+      const ItemGeom it = item_geom<C>(a, item);
       const int x0 = a.g.off + it.ti0 - 2, y0 = it.tj0 - 2;
       for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl, ++e) {
         if (e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[s], ph ^ 1);
@@ -298,10 +306,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     for (long long item = blockIdx.x; item < total; item += G) {
-      const ItemGeom it = item_geom(a, item);
+      const ItemGeom it = item_geom<C>(a, item);
       for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl) {
         tma::mbar_wait(&full[s], ph);
-        patch_plane(ring + s * kTmaSlot, a, it, pl, pc, lane);
+        patch_plane<Cfg::BH>(ring + s * kTmaSlot, a, it, pl, pc, lane);
         tma::fence_proxy_async();  // generic writes before the slot's next TMA fill
         __syncwarp();
         if (lane == 0) tma::mbar_arrive(&ready[s]);
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   };
 
   for (long long item = blockIdx.x; item < total; item += G) {
-    const ItemGeom it = item_geom(a, item);
+    const ItemGeom it = item_geom<C>(a, item);
     const int len = it.ke - it.kb;
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];

@@ -1,4 +1,4 @@
-"""Repeat the np=4 1d-i v2 overlap case on one GPU, timing each run."""
+"""Repeat np=4 1d-i overlap runs on one GPU under both comm-stream priorities."""
 import os
 import sys
 import time
@@ -9,17 +9,17 @@ import torch  # noqa: E402
 from paper_2006_02602_b200 import capi  # noqa: E402
 
 torch.cuda.init()
-for kern in ("tma", "tiled"):
-    os.environ["CAV_STEP_KERNEL"] = kern
+for prio in ("0", "1"):
+    os.environ["CAV_COMM_PRIORITY"] = prio
+    fails = 0
     for strat in ("baseline", "v1", "v2", "v3"):
-        for ov in (0, 1):
-            for rep in range(3):
-                cfg = capi.default_config(grid=(20, 16, 16), steps=10, np=4, mode="1d-i", strategy=strat,
-                                          overlap=ov, timeout_ms=4000)
-                t = time.time()
-                try:
-                    capi.run_case(cfg, collect_fields=True)
-                    res = "ok"
-                except Exception as e:
-                    res = repr(e)[:120]
-                print(f"{kern} {strat} ov={ov} rep={rep} {time.time()-t:.3f}s {res}", flush=True)
+        for rep in range(6):
+            cfg = capi.default_config(grid=(20, 16, 16), steps=10, np=4, mode="1d-i", strategy=strat,
+                                      overlap=1, timeout_ms=3000)
+            t = time.time()
+            try:
+                capi.run_case(cfg, collect_fields=True)
+            except Exception as e:
+                fails += 1
+                print(f"prio={prio} {strat} rep={rep} {time.time()-t:.3f}s {repr(e)[:110]}", flush=True)
+    print(f"prio={prio}: {fails} failures of 24", flush=True)
