@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
       a.state[v * a.g.fstride + a.g.idx(i, j, k)] = x;
     }
   }
+  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgUnpackDone, a.n);
 }
 
 // ---------------------------------------------------------------------------
@@ -706,8 +707,8 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int bh) {
 
 // TMA step variants (tile height, ring depth, CTAs per SM); CAV_TMA_CFG picks
 // one for experiments, variant 0 is the default.
-using TmaV0 = TmaCfg<16, 7, 1>;
-using TmaV1 = TmaCfg<8, 6, 2>;
+using TmaV0 = TmaCfg<8, 6, 2>;  // measured best on B200 (sweep in profiles/)
+using TmaV1 = TmaCfg<16, 7, 1>;
 using TmaV2 = TmaCfg<8, 12, 1>;
 using TmaV3 = TmaCfg<12, 9, 1>;
 constexpr int kTmaVariants = 4;

@@ -269,6 +269,20 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
         });
       for (auto& t : threads) t.join();
     }
+    if (std::getenv("CAV_DEBUG_DUMP")) {  // diagnostics: progress stamps of every rank
+      for (int r = 0; r < sh.np; ++r) {
+        if (!sh.blocks[r]) continue;
+        std::vector<uint64_t> v(130 + 16 * sh.np + 7);
+        if (cav_block_debug(sh.blocks[r], v.data(), static_cast<int>(v.size())) != CAV_OK) continue;
+        std::fprintf(stderr, "rank %d flags", r);
+        for (int q = 0; q < 6; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[q]);
+        std::fprintf(stderr, " | stamps");
+        for (int q = 0; q < 2 * sh.np; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[64 + 8 * q + 5]);
+        std::fprintf(stderr, " | progress");
+        for (int q = 0; q < 7; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[130 + 16 * sh.np + q]);
+        std::fprintf(stderr, "\n");
+      }
+    }
     for (auto* b : sh.blocks)
       if (b) cav_block_destroy(b);
     // prefer the root cause over "aborted by" echoes (src/runner.cpp:294-309)

@@ -4,12 +4,13 @@ import sys
 import time
 
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ["CAV_DEBUG_DUMP"] = "1"
 sys.path.insert(0, ".")
 import torch  # noqa: E402
 from paper_2006_02602_b200 import capi  # noqa: E402
 
 torch.cuda.init()
-for prio in ("0", "1"):
+for prio in ("0",):
     os.environ["CAV_COMM_PRIORITY"] = prio
     fails = 0
     for strat in ("baseline", "v1", "v2", "v3"):
