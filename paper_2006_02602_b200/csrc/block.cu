@@ -29,6 +29,8 @@
 
 #include <cudaTypedefs.h>
 
+#include <chrono>
+
 #include <cstdlib>
 
 #include "device.cuh"
@@ -782,6 +784,7 @@ struct Block {
   WallInfo winfo{};
   int tma_grid = 0;
   int tma_variant = 0;
+  double host_marks[6] = {};  // diagnostics: host timestamps inside the first run (s)
   bool use_tma = true;
 
   explicit Block(const cav_block_desc& desc);
@@ -1371,9 +1374,15 @@ int cav_block_download(cav_block* bh, double* host5) {
   });
 }
 
+static double host_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int cav_block_run(cav_block* bh, cav_run_io* io) {
   return guarded([&] {
     Block& b = *bh->b;
+    const bool mark = io->first_it == 1;
+    if (mark) b.host_marks[0] = host_now();
     CAV_CUDA(cudaSetDevice(b.d.device));
     if (io->first_it != b.next_n)
       throw std::logic_error("block_run: iterations must continue at " + std::to_string(b.next_n));
@@ -1381,6 +1390,7 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       throw std::runtime_error("iteration " + std::to_string(io->first_it) + ": compute_dt: cfl must be positive, got " +
                                host::fmt_double_f(b.d.cfl));
     b.ensure_ready();
+    if (mark) b.host_marks[1] = host_now();
     const long long first = io->first_it, last = io->first_it + io->n_its - 1;
     const int cadence = std::max(1, io->check_every);
     auto is_check = [&](long long it) { return io->want_norms && (it == 1 || it % cadence == 0); };
@@ -1395,6 +1405,7 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     }
     if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
     if (!b.primed) b.prologue();
+    if (mark) b.host_marks[2] = host_now();
     bool started = false;
     if (first != 1) {
       CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
@@ -1407,6 +1418,7 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       if (chk && io->check_iters) io->check_iters[ci] = it;
       ci += chk;
       b.iteration(it, chk, dig, false);
+      if (mark && it == 1) b.host_marks[3] = host_now();
       b.update_ledger(io->ledger);
       if (it == 1) {  // iteration 1 is warm-up (src/runner.cpp:186)
         CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
@@ -1414,7 +1426,9 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       }
     }
     CAV_CUDA(cudaEventRecord(b.ev_b, b.s0));
+    if (mark) b.host_marks[4] = host_now();
     CAV_CUDA(cudaStreamSynchronize(b.s0));
+    if (mark) b.host_marks[5] = host_now();
     float ms = 0.f;
     if (started && io->n_its > 0) CAV_CUDA(cudaEventElapsedTime(&ms, b.ev_a, b.ev_b));
     io->seconds = ms * 1e-3;
@@ -1452,13 +1466,14 @@ int cav_block_debug(cav_block* bh, uint64_t* out, int cap) {
     CAV_CUDA(cudaSetDevice(b.d.device));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s1));
-    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64 + kDbgStages);
+    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64 + kDbgStages + 6);
     CAV_CUDA(cudaMemcpy(v.data(), b.arena, (64 + 16 * b.d.np) * 8, cudaMemcpyDeviceToHost));
     CAV_CUDA(cudaMemcpy(v.data() + 64 + 16 * b.d.np, b.err, 16, cudaMemcpyDeviceToHost));
     std::vector<unsigned> c(64);
     CAV_CUDA(cudaMemcpy(c.data(), b.counters, 64 * 4, cudaMemcpyDeviceToHost));
     for (int q = 0; q < 64; ++q) v[66 + 16 * b.d.np + q] = c[q];
     CAV_CUDA(cudaMemcpy(v.data() + 130 + 16 * b.d.np, b.dbg, kDbgStages * 8, cudaMemcpyDeviceToHost));
+    std::memcpy(v.data() + 130 + 16 * b.d.np + kDbgStages, b.host_marks, sizeof b.host_marks);
     for (size_t q = 0; q < v.size() && static_cast<int>(q) < cap; ++q) out[q] = v[q];
   });
 }

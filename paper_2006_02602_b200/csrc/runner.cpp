@@ -272,7 +272,7 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
     if (std::getenv("CAV_DEBUG_DUMP")) {  // diagnostics: progress stamps of every rank
       for (int r = 0; r < sh.np; ++r) {
         if (!sh.blocks[r]) continue;
-        std::vector<uint64_t> v(130 + 16 * sh.np + 7);
+        std::vector<uint64_t> v(130 + 16 * sh.np + 7 + 6);
         if (cav_block_debug(sh.blocks[r], v.data(), static_cast<int>(v.size())) != CAV_OK) continue;
         std::fprintf(stderr, "rank %d flags", r);
         for (int q = 0; q < 6; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[q]);
@@ -280,7 +280,11 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
         for (int q = 0; q < 2 * sh.np; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[64 + 8 * q + 5]);
         std::fprintf(stderr, " | progress");
         for (int q = 0; q < 7; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[130 + 16 * sh.np + q]);
-        std::fprintf(stderr, "\n");
+        double hm[6];
+        std::memcpy(hm, v.data() + 137 + 16 * sh.np, sizeof hm);
+        std::fprintf(stderr, " | host ms: ready %.3f prologue %.3f it1 %.3f enq %.3f sync %.3f (t0 %.6f)\n",
+                     1e3 * (hm[1] - hm[0]), 1e3 * (hm[2] - hm[0]), 1e3 * (hm[3] - hm[0]), 1e3 * (hm[4] - hm[0]),
+                     1e3 * (hm[5] - hm[0]), hm[0]);
       }
     }
     for (auto* b : sh.blocks)
