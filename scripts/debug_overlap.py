@@ -4,7 +4,8 @@ import sys
 import time
 
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-os.environ["CAV_DEBUG_DUMP"] = "1"
+print("CUDA_DEVICE_MAX_CONNECTIONS", os.environ["CUDA_DEVICE_MAX_CONNECTIONS"], flush=True)
+
 sys.path.insert(0, ".")
 import torch  # noqa: E402
 from paper_2006_02602_b200 import capi  # noqa: E402
