@@ -784,6 +784,7 @@ struct Block {
   WallInfo winfo{};
   int tma_grid = 0;
   int tma_variant = 0;
+  bool two_streams = false;  // CAV_OVERLAP_STREAMS=2
   double host_marks[6] = {};  // diagnostics: host timestamps inside the first run (s)
   bool use_tma = true;
 
@@ -869,6 +870,8 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");
     use_tma = !(k && std::string(k) == "tiled");
+    const char* os = std::getenv("CAV_OVERLAP_STREAMS");
+    two_streams = os && std::atoi(os) == 2;
     const char* v = std::getenv("CAV_TMA_CFG");
     tma_variant = v ? std::max(0, std::min(kTmaVariants - 1, std::atoi(v))) : 0;
     switch (tma_variant) {
@@ -1163,9 +1166,28 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
     if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
     launch_step(ib, it, check, dig);
     if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+  } else if (!two_streams) {
+    // overlap (src/runner.cpp:189-194) in the reference's own order:
+    // exchange_begin (pack = remote stores into the neighbours' slabs),
+    // internal box, exchange_finish (acquire + unpack), external shells. The
+    // neighbours' pushes into our slabs travel while the internal box
+    // computes, so the transfer is hidden without a second stream (and
+    // without cross-stream events, which can serialise ranks sharing a GPU).
+    x.msg = d_pack;
+    k_pack<<<xgrid, kXThreads, 0, s0>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
+    launch_step(internal, it, check, dig);
+    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+    x.msg = d_unpack;
+    k_wait_flags<<<1, 32, 0, s0>>>(x, static_cast<int>(plan.size()));
+    CAV_CUDA(cudaGetLastError());
+    k_unpack<<<xgrid, kXThreads, 0, s0>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    launch_shells(it, check, dig);
   } else {
-    // overlap (src/runner.cpp:189-194): exchange on the high-priority comm
-    // stream while the internal box computes; shells after the join
+    // two-stream overlap: pack/wait/unpack on the comm stream concurrently
+    // with the internal box, shells after the join
     CAV_CUDA(cudaEventRecord(ev_fork, s0));
     CAV_CUDA(cudaStreamWaitEvent(s1, ev_fork, 0));
     x.msg = d_pack;
@@ -1484,7 +1506,7 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
   int n = (walls && !b.use_tma ? 1 : 0) + 1 + 1;  // [bc], step, sync
-  if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);
+  if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);  // pack, wait, unpack, [shells]
   return n;
 }
 
