@@ -1064,6 +1064,18 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     }
     a.nchunks = (bd + a.chunk - 1) / a.chunk;
     a.walls = winfo;
+    a.fold = d.np == 1 ? 1 : 0;
+    a.done = counters + 63;
+    a.sc_next = sc + ((it + 1) & 1);
+    a.acc_next = acc + ((it + 1) & 1);
+    a.err_sticky = err;
+    a.dx = dx;
+    a.dy = dy;
+    a.dz = dz;
+    a.cfl = d.cfl;
+    a.nu = d.fluid.nu;
+    a.alpha = d.fluid.alpha;
+    a.rescale = d.rescale;
     const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
     const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
     switch (tma_variant) {
@@ -1204,6 +1216,10 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
     if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
     CAV_CUDA(cudaStreamWaitEvent(s0, ev_join, 0));
     launch_shells(it, check, dig);
+  }
+  if (use_tma && d.np == 1) {  // the step kernel's last CTA folded the scalars
+    cur ^= 1;
+    return;
   }
   SyncArgs a{};
   a.dbg = dbg;
@@ -1505,7 +1521,7 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   (void)check;
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
-  int n = (walls && !b.use_tma ? 1 : 0) + 1 + 1;  // [bc], step, sync
+  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (b.use_tma && b.d.np == 1 ? 0 : 1);  // [bc], step, [sync]
   if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);  // pack, wait, unpack, [shells]
   return n;
 }

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include "device.cuh"
+#include "ops.hpp"
 
 namespace cav {
 
@@ -101,6 +102,15 @@ struct TmaStepArgs {
   int rank;
   int tiles_x, ntiles, chunk, nchunks;
   WallInfo walls;
+  // single-rank fold (replaces k_scalar_sync when np == 1): the last CTA to
+  // finish turns this iteration's maxima into dt_{n+1} and publishes pc_n
+  int fold;
+  unsigned* done;
+  IterScalars* sc_next;
+  Acc* acc_next;
+  unsigned long long* err_sticky;
+  double dx, dy, dz, cfl, nu, alpha;
+  int rescale;
 };
 
 struct ItemGeom {
@@ -493,6 +503,25 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
     acc_publish(a.acc, m0, m1, m2, mk & 0xFF, a.n + 1, a.rank);
     if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
+    if (a.fold) {
+      __threadfence();
+      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {  // every CTA has published
+        __threadfence();
+        volatile Acc* acc = a.acc;
+        const unsigned long long dm[3] = {acc->dmax[0], acc->dmax[1], acc->dmax[2]};
+        cav_fluid_params fl{};
+        fl.nu = a.nu;
+        fl.alpha = a.alpha;
+        a.sc_next->dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, fl, a.cfl);
+        a.sc_next->pc = a.rescale ? acc->pc_local : 0.0;
+        const unsigned long long e = acc->err;
+        if (e < *a.err_sticky) *a.err_sticky = e;
+        Acc z{};
+        z.err = ~0ull;
+        *a.acc_next = z;
+        *a.done = 0;
+      }
+    }
   }
   if (NORMS)
     for (int x = threadIdx.x; x < 5 * kDigits; x += NC)
