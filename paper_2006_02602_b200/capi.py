@@ -154,8 +154,9 @@ class CaseResult:
         return getattr(self, k)
 
 
-def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=False):
-    """run_case (src/runner.cpp:259-338) on the GPU(s) in cfg.devices."""
+def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=False, fmad=False):
+    """run_case (src/runner.cpp:259-338) on the GPU(s) in cfg.devices.
+    fmad=True uses the tolerance build (FMA contraction; not bitwise)."""
     n = cfg.nx * cfg.ny * cfg.nz
     fields = np.zeros(5 * n) if collect_fields else None
     target = cfg.steps if cfg.steps >= 0 else cfg.max_steps
@@ -172,7 +173,8 @@ def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=
     out.ledger_capacity = nl
     out.ledgers = C.cast(led, C.POINTER(A.Ledger))
     opt = A.CaseOptions(int(collect_fields), int(collect_history), int(corrupt_exchange))
-    check(lib().cav_run_case(C.byref(cfg), C.byref(opt), C.byref(out)))
+    L = lib(fmad)
+    check(L.cav_run_case(C.byref(cfg), C.byref(opt), C.byref(out)), L)
     h = int(out.hist_count)
     return CaseResult(
         steps_marched=out.steps_marched, steps_timed=out.steps_timed,

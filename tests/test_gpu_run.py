@@ -192,3 +192,18 @@ def test_fused_step_large_block_matches_oracle():
     o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
     np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+
+
+@pytest.mark.parametrize("name", ["r16x12x9_200", "ra1e4_20x16x12_120"])
+def test_fmad_tolerance_build_within_1e10(golden, golden_arrays, name):
+    """The FMA-contracted build (libcavity_b200_fmad.so) is not bitwise, but
+    stays within BASELINE.json's 1e-10 relative tolerance (compare_fields
+    metric, src/runner.cpp:355-375) on fields and the norm history."""
+    entry = golden["runs"][name]
+    cfg = golden_config(entry, capi.default_config)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True, fmad=True)
+    rep = capi.compare_fields(golden_arrays["runs"][name], r.fields, 1e-10)
+    assert rep.passed, rep.summary()
+    want = np.array([[float.fromhex(x) for x in row] for row in entry["history"]])
+    rel = np.abs(r.history - want) / np.maximum(np.abs(want), 1e-300)
+    assert np.all(rel[want != 0] <= 1e-10)
