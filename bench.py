@@ -288,7 +288,7 @@ def run_ours(args):
     tkey = f"{grid[0]}x{grid[1]}x{grid[2]}"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": (traffic or {}).get(tkey),
-            "kernel": "k_step_tiled (fused residual+update+dt+rescale)",
+            "kernel": "k_step_tma (TMA-fed fused BC+residual+update+dt+rescale)",
             "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells_local,
             "kernel_ms": step_ms, "peak_source": peak_src,
             "step_share": step_ms * args.steps / total_ms if total_ms > 0 else None}

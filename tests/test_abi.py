@@ -57,3 +57,31 @@ def test_product_does_not_import_the_oracle():
 def test_sm100a_cubin_in_library():
     data = open(capi.lib_path(), "rb").read()
     assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_cpp_header_rethrows_reference_exceptions(tmp_path):
+    """include/cavity_b200.hpp maps status codes back onto the reference's
+    exception types and messages (compiled and run here, host logic only)."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        return
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "cavity_b200.hpp"
+int main() {
+  int d[3];
+  try { cavity_b200::check(cav_choose_dims(7, CAV_MODE_2D, d)); return 1; }
+  catch (const std::invalid_argument& e) { std::printf("%s\n", e.what()); }
+  cavity_b200::check(cav_choose_dims(8, CAV_MODE_3D, d));
+  std::printf("%d %d %d\n", d[0], d[1], d[2]);
+  return 0;
+}''')
+    exe = tmp_path / "t"
+    lib_dir = os.path.dirname(capi.lib_path())
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-L", lib_dir,
+                    "-lcavity_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines()
+    assert out[0].startswith("choose_dims: 2d cannot split a prime rank count 7")
+    assert out[1] == "2 2 2"
