@@ -70,6 +70,13 @@ __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int x
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(f), "r"(smem_u32(bar))
       : "memory");
 }
+// L2-only prefetch of one box (no shared-memory destination, no completion).
+__device__ __forceinline__ void prefetch_4d(const CUtensorMap* map, int x, int y, int z, int f) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(f)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -78,6 +85,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }  // namespace tma
 
 constexpr int kTmaBW = 36;  // 32 + 2x2 halo
+constexpr int kPrefetch = 8;       // L2 prefetch distance, in plane entries
 
 // Tile height TY (= consumer warps), ring depth R and CTAs per SM.
 template <int TY_, int R_, int CTAS_>
@@ -294,13 +302,37 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
 
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
+    // A second cursor runs kPrefetch entries ahead and pulls those planes
+    // into L2 (no smem), so the ring's own loads hit L2 instead of waiting
+    // out DRAM latency with only R-3 slots in flight.
     if (lane != 0) return;
     int s = 0;
     uint32_t ph = 0, e = 0;  // slot / empty-barrier phase of entry e
+    long long pf_item = blockIdx.x;
+    ItemGeom pf{0, 0, 0, 0};
+    int pf_pl = 0;
+    if (pf_item < total) {
+      pf = item_geom<C>(a, pf_item);
+      pf_pl = pf.kb - 2;
+    }
+    auto prefetch_next = [&]() {
+      if (pf_item >= total) return;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) tma::prefetch_4d(&map, a.g.off + pf.ti0 - 2, pf.tj0 - 2, pf_pl, f);
+      if (++pf_pl > pf.ke + 1) {
+        pf_item += G;
+        if (pf_item < total) {
+          pf = item_geom<C>(a, pf_item);
+          pf_pl = pf.kb - 2;
+        }
+      }
+    };
+    for (int q = 0; q < kPrefetch; ++q) prefetch_next();
     for (long long item = blockIdx.x; item < total; item += G) {
       const ItemGeom it = item_geom<C>(a, item);
       const int x0 = a.g.off + it.ti0 - 2, y0 = it.tj0 - 2;
       for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl, ++e) {
+        prefetch_next();
         if (e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[s], ph ^ 1);
         tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
         double* dst = ring + s * kTmaSlot;
