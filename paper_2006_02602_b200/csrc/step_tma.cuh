@@ -368,6 +368,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   }
 
   // ---------------- consumers ----------------
+  // Each step computes two planes (k, k+1) of the thread's column: the
+  // k-windows are shared (p: k-2..k+3, u,v,w,T: k-1..k+2), waits/releases and
+  // loop control are paid once per two cells, and the two independent
+  // residuals interleave.
   const int tx = lane, ty = warp;
   const Geo g = a.g;
   const double dt = a.sc->dt, u_ref = a.sp.u_ref;
@@ -378,8 +382,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
   const double* ringc = ring + (ty + 2) * BW + tx + 2;  // own cell in slot 0, field 0
-  // rolling ring cursor: slot of the next entry to wait for, and its phase
-  int sw = 0;
+  int sw = 0;  // slot of the next entry to wait for, and its phase
   uint32_t phw = 0;
   auto advance = [&](int& sl, uint32_t& ph) {
     if (++sl == R) {
@@ -387,9 +390,93 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       ph ^= 1;
     }
   };
+  auto wait_next = [&]() {
+    const int sl = sw;
+    tma::mbar_wait(&ready[sw], phw);
+    advance(sw, phw);
+    return sl;
+  };
   auto release_slot = [&](int sl) {
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&empty[sl]);
+  };
+  auto slot = [&](int sl) { return ringc + sl * kTmaSlot; };
+
+  // z-wall ghosts inside the register windows (apply_boundary_conditions for
+  // the z walls). Two-plane step at k: P[0..5] = planes k-2..k+3,
+  // Q[f][0..3] = planes k-1..k+2; one-plane step: P[0..4], Q[f][0..2].
+  // Only compile-time indices, so the windows stay in registers.
+  auto qmirror = [&](double (*Q)[4], int gi, int ii) {  // ghost gi from interior ii
+    Q[0][gi] = -Q[0][ii];
+    Q[1][gi] = -Q[1][ii];
+    Q[2][gi] = -Q[2][ii];
+    Q[3][gi] = Q[3][ii];
+  };
+  auto zwall2 = [&](double* P, double (*Q)[4], int k) {
+    if (zlo && k == 2) {
+      P[1] = cubic_g0(P[2], P[3], P[4]);
+      P[0] = cubic_g1(P[1], P[2], P[3]);
+      qmirror(Q, 0, 1);
+    } else if (zlo && k == 3) {
+      P[0] = cubic_g0(P[1], P[2], P[3]);
+    }
+    if (zhi && k == g.nz - 1) {
+      P[5] = cubic_g0(P[4], P[3], P[2]);
+    } else if (zhi && k == g.nz) {
+      P[4] = cubic_g0(P[3], P[2], P[1]);
+      P[5] = cubic_g1(P[4], P[3], P[2]);
+      qmirror(Q, 3, 2);
+    }
+  };
+  auto zwall1 = [&](double* P, double (*Q)[4], int k) {
+    if (zlo && k == 2) {
+      P[1] = cubic_g0(P[2], P[3], P[4]);
+      P[0] = cubic_g1(P[1], P[2], P[3]);
+      qmirror(Q, 0, 1);
+    } else if (zlo && k == 3) {
+      P[0] = cubic_g0(P[1], P[2], P[3]);
+    }
+    if (zhi && k == g.nz) {
+      P[4] = cubic_g0(P[3], P[2], P[1]);
+    } else if (zhi && k == g.nz + 1) {
+      P[3] = cubic_g0(P[2], P[1], P[0]);
+      P[4] = cubic_g1(P[3], P[2], P[1]);
+      qmirror(Q, 2, 1);
+    }
+  };
+
+  // one cell: residual + update + store + bookkeeping
+  auto cell = [&](const double* B, double p0, double pzm, double pzp, double pzm2, double pzp2, const double* qc,
+                  const double* qm, const double* qp, double* op, bool ccolk) {
+    const SmemAcc sa{B, B + kTmaField, B + 2 * kTmaField, B + 3 * kTmaField, B + 4 * kTmaField,
+                     p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1], qp[1], qc[2], qm[2], qp[2],
+                     qc[3], qm[3], qp[3]};
+    const Res r = residual_t(sa, a.sp);
+    const double qpn = p0 + dt * r.p, qun = qc[0] + dt * r.u, qvn = qc[1] + dt * r.v, qwn = qc[2] + dt * r.w,
+                 qtn = qc[3] + dt * r.t;
+    op[0] = qpn;
+    op[fs] = qun;
+    op[2 * fs] = qvn;
+    op[3 * fs] = qwn;
+    op[4 * fs] = qtn;
+    const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref);
+    m0 = dmax_d(m0, d.du);
+    m1 = dmax_d(m1, d.dv);
+    m2 = dmax_d(m2, d.dw);
+    e_p = max(e_p, static_cast<unsigned>(__double2hiint(qpn)) & 0x7FF00000u);
+    e_u = max(e_u, static_cast<unsigned>(__double2hiint(qun)) & 0x7FF00000u);
+    e_v = max(e_v, static_cast<unsigned>(__double2hiint(qvn)) & 0x7FF00000u);
+    e_w = max(e_w, static_cast<unsigned>(__double2hiint(qwn)) & 0x7FF00000u);
+    e_t = max(e_t, static_cast<unsigned>(__double2hiint(qtn)) & 0x7FF00000u);
+    if (ccolk) a.acc->pc_local = qpn;
+    if (NORMS) {
+      const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        if (nonfinite(rr[v])) nbad = 1;
+        else add_term_digits(sdig + v * kDigits, rr[v]);
+      }
+    }
   };
 
   for (long long item = blockIdx.x; item < total; item += G) {
@@ -398,113 +485,81 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
     const bool ccol = i == a.cx && j == a.cy;
-    // prologue: entries for planes kb-2, kb-1, kb, kb+1
-    int s0 = sw;
-    tma::mbar_wait(&ready[sw], phw);
-    advance(sw, phw);
-    int s1 = sw;
-    tma::mbar_wait(&ready[sw], phw);
-    advance(sw, phw);
-    int s2 = sw;
-    tma::mbar_wait(&ready[sw], phw);
-    advance(sw, phw);
-    int s3 = sw;
-    tma::mbar_wait(&ready[sw], phw);
-    advance(sw, phw);
-    const double* B0 = ringc + s0 * kTmaSlot;
-    const double* B1 = ringc + s1 * kTmaSlot;
-    const double* B2 = ringc + s2 * kTmaSlot;
-    const double* B3 = ringc + s3 * kTmaSlot;
-    double pm2 = B0[0], pm1 = B1[0], p0 = B2[0], pp1 = B3[0];
-    double um1 = B1[kTmaField], u0 = B2[kTmaField];
-    double vm1 = B1[2 * kTmaField], v0 = B2[2 * kTmaField];
-    double wm1 = B1[3 * kTmaField], w0 = B2[3 * kTmaField];
-    double tm1 = B1[4 * kTmaField], t0 = B2[4 * kTmaField];
+    // prologue: planes kb-2 .. kb+1
+    const int s0 = wait_next(), s1 = wait_next(), s2 = wait_next(), s3 = wait_next();
+    double P[6];     // p at planes k-2 .. k+3
+    double Q[4][4];  // u,v,w,T at planes k-1 .. k+2
+    P[0] = slot(s0)[0];
+    P[1] = slot(s1)[0];
+    P[2] = slot(s2)[0];
+    P[3] = slot(s3)[0];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      Q[f][0] = slot(s1)[(f + 1) * kTmaField];
+      Q[f][1] = slot(s2)[(f + 1) * kTmaField];
+    }
     release_slot(s0);
     release_slot(s1);
-    // slots of planes k (cur) and k+1 (nxt); sw/phw = slot of plane k+2
-    int scur = s2, snxt = s3;
+    int sc0 = s2, sc1 = s3;  // slots of planes k, k+1
     double* op = a.out + g.idx(i, j, it.kb);
-    for (int st = 0; st < len; ++st, op += plane) {
+    int st = 0;
+    for (; st + 1 < len; st += 2, op += 2 * plane) {
       const int k = it.kb + st;
-      const int sk2 = sw;
-      tma::mbar_wait(&ready[sw], phw);
-      advance(sw, phw);
-      const double* Bc = ringc + scur * kTmaSlot;
-      const double* Bn = ringc + snxt * kTmaSlot;
-      double pp2 = (ringc + sk2 * kTmaSlot)[0];
-      double up1 = Bn[kTmaField], vp1 = Bn[2 * kTmaField], wp1 = Bn[3 * kTmaField], tp1 = Bn[4 * kTmaField];
-      // z-wall ghosts in the register window (uniform over the CTA)
-      if ((zlo && k <= 3) || (zhi && k >= g.nz)) {
-        if (zlo && k == 2) {
-          pm1 = cubic_g0(p0, pp1, pp2);
-          pm2 = cubic_g1(pm1, p0, pp1);
-          um1 = -u0;
-          vm1 = -v0;
-          wm1 = -w0;
-          tm1 = t0;
-        } else if (zlo && k == 3) {
-          pm2 = cubic_g0(pm1, p0, pp1);
-        }
-        if (zhi && k == g.nz) {
-          pp2 = cubic_g0(pp1, p0, pm1);
-        } else if (zhi && k == g.nz + 1) {
-          pp1 = cubic_g0(p0, pm1, pm2);
-          pp2 = cubic_g1(pp1, p0, pm1);
-          up1 = -u0;
-          vp1 = -v0;
-          wp1 = -w0;
-          tp1 = t0;
-        }
-      }
-      if (active) {
-        const SmemAcc sa{Bc, Bc + kTmaField, Bc + 2 * kTmaField, Bc + 3 * kTmaField, Bc + 4 * kTmaField,
-                         p0, pm1, pp1, pm2, pp2, u0, um1, up1, v0, vm1, vp1, w0, wm1, wp1, t0, tm1, tp1};
-        const Res r = residual_t(sa, a.sp);
-        const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
-                     qt = t0 + dt * r.t;
-        op[0] = qp;
-        op[fs] = qu;
-        op[2 * fs] = qv;
-        op[3 * fs] = qw;
-        op[4 * fs] = qt;
-        const Denoms d = cfl_denoms(qu, qv, qw, u_ref);
-        m0 = dmax_d(m0, d.du);
-        m1 = dmax_d(m1, d.dv);
-        m2 = dmax_d(m2, d.dw);
-        e_p = max(e_p, static_cast<unsigned>(__double2hiint(qp)) & 0x7FF00000u);
-        e_u = max(e_u, static_cast<unsigned>(__double2hiint(qu)) & 0x7FF00000u);
-        e_v = max(e_v, static_cast<unsigned>(__double2hiint(qv)) & 0x7FF00000u);
-        e_w = max(e_w, static_cast<unsigned>(__double2hiint(qw)) & 0x7FF00000u);
-        e_t = max(e_t, static_cast<unsigned>(__double2hiint(qt)) & 0x7FF00000u);
-        if (ccol && k == a.cz) a.acc->pc_local = qp;
-        if (NORMS) {
-          const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
+      const int sc2 = wait_next(), sc3 = wait_next();  // planes k+2, k+3
+      P[4] = slot(sc2)[0];
+      P[5] = slot(sc3)[0];
 #pragma unroll
-          for (int v = 0; v < 5; ++v) {
-            if (nonfinite(rr[v])) nbad = 1;
-            else add_term_digits(sdig + v * kDigits, rr[v]);
-          }
-        }
+      for (int f = 0; f < 4; ++f) {
+        Q[f][2] = slot(sc1)[(f + 1) * kTmaField];
+        Q[f][3] = slot(sc2)[(f + 1) * kTmaField];
       }
-      release_slot(scur);
-      scur = snxt;
-      snxt = sk2;
-      pm2 = pm1;
-      pm1 = p0;
-      p0 = pp1;
-      pp1 = pp2;
-      um1 = u0;
-      u0 = up1;
-      vm1 = v0;
-      v0 = vp1;
-      wm1 = w0;
-      w0 = wp1;
-      tm1 = t0;
-      t0 = tp1;
+      if ((zlo && k <= 3) || (zhi && k + 3 >= g.nz + 2)) zwall2(P, Q, k);
+      if (active) {
+        const double qa[4] = {Q[0][1], Q[1][1], Q[2][1], Q[3][1]};
+        const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
+        const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
+        const double qbp[4] = {Q[0][3], Q[1][3], Q[2][3], Q[3][3]};
+        cell(slot(sc0), P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
+        cell(slot(sc1), P[3], P[2], P[4], P[1], P[5], qap, qa, qbp, op + plane, ccol && k + 1 == a.cz);
+      }
+      release_slot(sc0);
+      release_slot(sc1);
+      sc0 = sc2;
+      sc1 = sc3;
+      P[0] = P[2];
+      P[1] = P[3];
+      P[2] = P[4];
+      P[3] = P[5];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        Q[f][0] = Q[f][2];
+        Q[f][1] = Q[f][3];
+      }
     }
-    release_slot(scur);  // planes ke, ke+1 served only as column values
-    release_slot(snxt);
+    if (st < len) {  // odd remainder: one plane
+      const int k = it.kb + st;
+      const int sc2 = wait_next();  // plane k+2
+      P[4] = slot(sc2)[0];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) Q[f][2] = slot(sc1)[(f + 1) * kTmaField];
+      if ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2)) zwall1(P, Q, k);
+      if (active) {
+        const double qa[4] = {Q[0][1], Q[1][1], Q[2][1], Q[3][1]};
+        const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
+        const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
+        cell(slot(sc0), P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
+      }
+      release_slot(sc0);
+      sc0 = sc1;
+      sc1 = sc2;
+      // remaining entries: plane k+1 (sc0 now) was waited; plane k+2 (sc1) waited
+      release_slot(sc0);
+      release_slot(sc1);
+    } else {
+      // planes ke, ke+1 (sc0, sc1) served only as column values
+      release_slot(sc0);
+      release_slot(sc1);
+    }
   }
   constexpr unsigned EXP = 0x7FF00000u;
   unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
