@@ -454,11 +454,13 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const Res r = residual_t(sa, a.sp);
     const double qpn = p0 + dt * r.p, qun = qc[0] + dt * r.u, qvn = qc[1] + dt * r.v, qwn = qc[2] + dt * r.w,
                  qtn = qc[3] + dt * r.t;
-    op[0] = qpn;
-    op[fs] = qun;
-    op[2 * fs] = qvn;
-    op[3 * fs] = qwn;
-    op[4 * fs] = qtn;
+    // explicit global (streaming) stores: no possible aliasing with the
+    // shared-memory ring, so the two cells of a step can interleave
+    __stcs(op, qpn);
+    __stcs(op + fs, qun);
+    __stcs(op + 2 * fs, qvn);
+    __stcs(op + 3 * fs, qwn);
+    __stcs(op + 4 * fs, qtn);
     const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref);
     m0 = dmax_d(m0, d.du);
     m1 = dmax_d(m1, d.dv);
