@@ -52,6 +52,7 @@ struct StepArgs {
   double* out;
   Geo g;
   cav_stencil_params sp;
+  double s2fast;  // beta shortcut threshold (host::beta_fast_s2)
   cav_box box;
   int kchunk;
   const IterScalars* sc;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
       st.typ = BT[QW];
       st.tzm = tm1;
       st.tzp = tp1;
-      const Res r = residual_of(st, a.sp);
+      const Res r = residual_of(st, a.sp, a.s2fast);
       // euler_step: q = q + dt*r (src/solver.cpp:239-246)
       const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
                    qt = t0 + dt * r.t;
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
       out[2 * fs + c] = qv;
       out[3 * fs + c] = qw;
       out[4 * fs + c] = qt;
-      const Denoms d = cfl_denoms(qu, qv, qw, u_ref);
+      const Denoms d = cfl_denoms(qu, qv, qw, u_ref, a.s2fast);
       m0 = dmax_d(m0, d.du);
       m1 = dmax_d(m1, d.dv);
       m2 = dmax_d(m2, d.dw);
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a
     const double pc = s.sc->pc, dt = s.sc->dt;
     Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
     if (near_wall(a.walls, g, i, j, k)) apply_wall_ghosts(st, a.walls, g, i, j, k);
-    const Res r = residual_of(st, s.sp);
+    const Res r = residual_of(st, s.sp, s.s2fast);
     const double qp = st.p + dt * r.p, qu = st.u + dt * r.u, qv = st.v + dt * r.v, qw = st.w + dt * r.w,
                  qt = st.t + dt * r.t;
     const long long c = g.idx(i, j, k);
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a
     s.out[2 * fs + c] = qv;
     s.out[3 * fs + c] = qw;
     s.out[4 * fs + c] = qt;
-    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref);
+    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref, s.s2fast);
     m0 = d.du;
     m1 = d.dv;
     m2 = d.dw;
@@ -676,6 +677,18 @@ cudaEvent_t make_event() {
 
 }  // namespace
 
+// pcs_1 = p'(centre) of the first step (eager mode; later ones are folded by
+// the step kernel's last CTA).
+__global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, double s2fast,
+                             IterScalars* sc, int cx, int cy, int cz) {
+  if (threadIdx.x == 0) sc->pcs = center_p_update(state, g, w, sp, s2fast, sc->dt, 0.0, cx, cy, cz);
+}
+
+int getenv_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -688,16 +701,18 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// 4-D view (x = padded row, y, z, field) of one 5-field state for TMA; box =
-// one 36 x (TY+4) plane tile of one field.
-CUtensorMap make_state_map(const double* base, const Geo& g, int bh) {
+// 4-D views (x = padded row, y, z, field) of one 5-field state for TMA:
+// `p` = field 0 with a 36 x (TY+4) box, `q` = fields 1..4 (u, v, w, T) with a
+// 34 x (TY+2) x 1 x 4 box (one TMA per plane for all four).
+CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw, int bh) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(g.ypitch),
-                              static_cast<cuuint64_t>(g.nz + 4), 5};
+                              static_cast<cuuint64_t>(g.nz + 4), static_cast<cuuint64_t>(nfields)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.pitch) * 8,
                                  static_cast<cuuint64_t>(g.pitch) * g.ypitch * 8,
                                  static_cast<cuuint64_t>(g.fstride) * 8};
-  const cuuint32_t box[4] = {kTmaBW, static_cast<cuuint32_t>(bh), 1, 1};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1,
+                             static_cast<cuuint32_t>(nfields)};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -709,10 +724,10 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int bh) {
 
 // TMA step variants (tile height, ring depth, CTAs per SM); CAV_TMA_CFG picks
 // one for experiments, variant 0 is the default.
-using TmaV0 = TmaCfg<8, 6, 2>;  // measured best on B200 (sweep in profiles/)
-using TmaV1 = TmaCfg<16, 7, 1>;
-using TmaV2 = TmaCfg<8, 12, 1>;
-using TmaV3 = TmaCfg<12, 9, 1>;
+using TmaV0 = TmaCfg<12, 10, 1>;  // default: 13 warps -> 128 registers, 6 slots in flight
+using TmaV1 = TmaCfg<8, 7, 2>;
+using TmaV2 = TmaCfg<8, 14, 1>;
+using TmaV3 = TmaCfg<16, 8, 1>;
 constexpr int kTmaVariants = 4;
 constexpr int kTmaVariantTY[kTmaVariants] = {TmaV0::TY, TmaV1::TY, TmaV2::TY, TmaV3::TY};
 
@@ -734,9 +749,9 @@ int tma_setup(int device) {
 }
 
 template <class Cfg>
-void tma_launch(const CUtensorMap& m, const TmaStepArgs& a, bool check, int grid, cudaStream_t st) {
-  if (check) k_step_tma<Cfg, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m, a);
-  else k_step_tma<Cfg, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m, a);
+void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, int grid, cudaStream_t st) {
+  if (check) k_step_tma<Cfg, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+  else k_step_tma<Cfg, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
   CAV_CUDA(cudaGetLastError());
 }
 
@@ -780,7 +795,9 @@ struct Block {
   std::vector<cudaEvent_t> kev;  // bench: per-step kernel timing
   int kind_ty = 8;
   int kchunk = 0;
-  CUtensorMap tmap[2];
+  CUtensorMap tmap[2][2];  // [state][p, uvwT]
+  double s2fast = -1.0;
+  bool eager = false;            // single-rank TMA pipeline: rescaled p stored directly
   WallInfo winfo{};
   int tma_grid = 0;
   int tma_variant = 0;
@@ -826,6 +843,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     cz = c[2] - e.lo[2] + 2;
   }
   sp = host::stencil_params(dx, dy, dz, d.fluid);
+  s2fast = host::beta_fast_s2(sp.u_ref);
   plan = host::build_plan(n, rank_at, d.strategy);
   host::overlap_regions(n, rank_at, &internal, shells);
   lay = arena_layout(plan, d.np);
@@ -866,10 +884,13 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_scalar_sync));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_center_pcs));
   }
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");
     use_tma = !(k && std::string(k) == "tiled");
+    const char* ea = std::getenv("CAV_EAGER");
+    eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
     const char* os = std::getenv("CAV_OVERLAP_STREAMS");
     two_streams = os && std::atoi(os) == 2;
     const char* v = std::getenv("CAV_TMA_CFG");
@@ -880,7 +901,11 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
       case 3: tma_grid = tma_setup<TmaV3>(d.device); break;
       default: tma_grid = tma_setup<TmaV0>(d.device); break;
     }
-    for (int s = 0; s < 2; ++s) tmap[s] = make_state_map(state[s], g, kTmaVariantTY[tma_variant] + 4);
+    const int ty = kTmaVariantTY[tma_variant];
+    for (int s = 0; s < 2; ++s) {
+      tmap[s][0] = make_state_map(state[s], g, 1, kPW, ty + 4);
+      tmap[s][1] = make_state_map(state[s] + g.fstride, g, 4, kQW, ty + 2);
+    }
   }
   CAV_CUDA(cudaMalloc(&arena, lay.bytes));
   // Stream-ordered and completed before any peer can see this arena: a
@@ -1025,17 +1050,25 @@ void Block::prologue() {
   a.timeout_flag = tflag;
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
+  if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
+    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, s2fast, sc + 1, cx, cy, cz);
+    CAV_CUDA(cudaGetLastError());
+  }
   primed = true;
 }
 
 void Block::launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig) {
   const long long vol = host::box_volume(box);
   if (vol == 0) return;
-  if (use_tma) {
+  // TMA boxes must start 16-byte aligned along x (even FP64 element)
+  if (use_tma && ((g.off + box.lo[0]) & 1) == 0) {
     TmaStepArgs a{};
     a.out = state[cur ^ 1];
     a.g = g;
     a.sp = sp;
+    a.s2fast = s2fast;
+    a.work = counters + 62;
+    a.eager = eager ? 1 : 0;
     a.box = box;
     a.sc = sc + (it & 1);
     a.acc = acc + (it & 1);
@@ -1091,6 +1124,7 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
   a.out = state[cur ^ 1];
   a.g = g;
   a.sp = sp;
+  a.s2fast = s2fast;
   a.box = box;
   a.sc = sc + (it & 1);
   a.acc = acc + (it & 1);
@@ -1116,6 +1150,7 @@ void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
   a.s.out = state[cur ^ 1];
   a.s.g = g;
   a.s.sp = sp;
+  a.s.s2fast = s2fast;
   a.s.sc = sc + (it & 1);
   a.s.acc = acc + (it & 1);
   a.s.digits = dig;
@@ -1243,6 +1278,10 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
   a.timeout_flag = tflag;
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
+  if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
+    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, s2fast, sc + 1, cx, cy, cz);
+    CAV_CUDA(cudaGetLastError());
+  }
   cur ^= 1;
 }
 

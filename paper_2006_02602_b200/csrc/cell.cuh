@@ -37,11 +37,31 @@ struct Res {
 // its parenthesisation is the reference's; only the order in which independent
 // expressions are evaluated is grouped per equation, which keeps fewer values
 // live and cannot change any result.
+//
+// beta = max(sqrt(s2), u_ref) (compute_beta, include/cavity/solver.hpp:73-75).
+// `s2fast` is the largest double whose correctly rounded square root is still
+// below u_ref (host: beta_fast_s2); for s2 <= s2fast, beta is u_ref exactly
+// (sqrt is monotone), so the IEEE sqrt sequence is skipped. A negative s2fast
+// disables the shortcut; NaN s2 always takes the full path.
+// The square root is volatile inline PTX (sqrt.rn.f64, the same correctly
+// rounded operation) so the compiler cannot hoist it above the branch and
+// if-convert: at quiescent cells s2 == 0, which would otherwise run the IEEE
+// sequence's special-case call on every cell.
+__device__ __forceinline__ double sqrt_rn(double x) {
+  double r;
+  asm volatile("sqrt.rn.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double beta_of(double s2, double u_ref, double s2fast) {
+  double b = u_ref;
+  if (!(s2 <= s2fast)) b = smax(sqrt_rn(s2), u_ref);
+  return b;
+}
+
 template <class S>
-__device__ __forceinline__ Res residual_t(const S& s, const cav_stencil_params& q) {
+__device__ __forceinline__ Res residual_t(const S& s, const cav_stencil_params& q, double s2fast = -1.0) {
   const double uc = s.u(), vc = s.v(), wc = s.w(), tc = s.t();
-  const double speed = sqrt((uc * uc + vc * vc) + wc * wc);
-  const double b = smax(speed, q.u_ref);
+  const double b = beta_of((uc * uc + vc * vc) + wc * wc, q.u_ref, s2fast);
   const double b2 = b * b;
   Res r;
   // continuity + fourth-difference damping
@@ -121,8 +141,8 @@ struct StarAcc {
 #undef CAV_A
 };
 
-__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q) {
-  return residual_t(StarAcc{s}, q);
+__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q, double s2fast = -1.0) {
+  return residual_t(StarAcc{s}, q, s2fast);
 }
 
 // compute_beta (include/cavity/solver.hpp:73-75) and the per-cell CFL
@@ -133,8 +153,8 @@ __device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_para
 struct Denoms {
   double du, dv, dw;
 };
-__device__ __forceinline__ Denoms cfl_denoms(double u, double v, double w, double u_ref) {
-  const double b = smax(sqrt((u * u + v * v) + w * w), u_ref);
+__device__ __forceinline__ Denoms cfl_denoms(double u, double v, double w, double u_ref, double s2fast = -1.0) {
+  const double b = beta_of((u * u + v * v) + w * w, u_ref, s2fast);
   return {fabs(u) + b, fabs(v) + b, fabs(w) + b};
 }
 

@@ -12,9 +12,15 @@ namespace cav {
 
 // Per-iteration scalars every kernel of iteration n reads: the step dt_n and
 // the pending centre-pressure shift pc_{n-1} (0 when rescale is off or n==1).
+// Eager mode (single-rank TMA pipeline) stores the rescaled pressure
+// directly: the updated p' of iteration n is written as fl(p' - pcs_n), where
+// pcs_n = p'(centre) is computed ahead of the step from the same inputs with
+// the same arithmetic (center_p_update). pc is then 0 (nothing pending).
 struct IterScalars {
   double dt;
-  double pc;
+  double pc;   // lazy shift consumers apply on load (pending pc_{n-1})
+  double pcs;  // eager shift the step applies on store (pc_n), else 0
+  double pad;
 };
 
 // Per-iteration accumulators written by the fused step (and the prologue scan).
@@ -171,6 +177,21 @@ __device__ __forceinline__ void apply_wall_ghosts(Star& s, const WallInfo& w, co
 __device__ __forceinline__ bool near_wall(const WallInfo& w, const Geo& g, int i, int j, int k) {
   return (w.wall[0] && i <= 3) || (w.wall[1] && i >= g.nx) || (w.wall[2] && j <= 3) ||
          (w.wall[3] && j >= g.ny) || (w.wall[4] && k <= 3) || (w.wall[5] && k >= g.nz);
+}
+
+// p' at one interior cell of `state` (layout g): the cell's residual and
+// Euler update exactly as the fused step computes them (compute_residual +
+// euler_step, src/solver.cpp:105-120, :234-246), with wall ghosts formed on
+// the fly. Used to obtain the centre pressure pc_n before the step that
+// stores fl(p' - pc_n) (rescale_pressure, src/solver.cpp:248-257).
+__device__ __forceinline__ double center_p_update(const double* state, const Geo& g, const WallInfo& w,
+                                                  const cav_stencil_params& sp, double s2fast, double dt,
+                                                  double pc_lazy, int i, int j, int k) {
+  const long long fs = g.fstride;
+  Star st = load_star(state, state + fs, state + 2 * fs, state + 3 * fs, state + 4 * fs, g, i, j, k, pc_lazy);
+  if (near_wall(w, g, i, j, k)) apply_wall_ghosts(st, w, g, i, j, k);
+  const Res r = residual_of(st, sp, s2fast);
+  return st.p + dt * r.p;
 }
 
 // Block-wide max of three doubles and OR of a mask; thread 0 gets the result.

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <stdexcept>
 
 #include "status.hpp"
@@ -124,6 +125,19 @@ cav_stencil_params stencil_params(double dx, double dy, double dz, const cav_flu
   s.gx = p.gravity[0];
   s.gy = p.gravity[1];
   s.gz = p.gravity[2];
+  return s;
+}
+
+double beta_fast_s2(double u_ref) {
+  if (!(u_ref > 0.0) || !std::isfinite(u_ref)) return -1.0;
+  const double inf = std::numeric_limits<double>::infinity();
+  double s = u_ref * u_ref;
+  while (s > 0.0 && !(std::sqrt(s) < u_ref)) s = std::nextafter(s, 0.0);
+  for (;;) {
+    const double t = std::nextafter(s, inf);
+    if (!(std::sqrt(t) < u_ref)) break;
+    s = t;
+  }
   return s;
 }
 

@@ -28,6 +28,10 @@ void validate_params(const cav_fluid_params& p);
 cav_fluid_params for_rayleigh(double ra);
 // make_stencil_params (src/solver.cpp:77-103).
 cav_stencil_params stencil_params(double dx, double dy, double dz, const cav_fluid_params& p);
+// Largest double s with sqrt(s) < u_ref (correctly rounded), so that
+// max(sqrt(s'), u_ref) == u_ref for every s' <= s; -1 when u_ref is not a
+// positive finite number (the device then always takes the full sqrt).
+double beta_fast_s2(double u_ref);
 
 // choose_dims (src/decomp.cpp:67-98).
 std::array<int, 3> choose_dims(int np, int mode);

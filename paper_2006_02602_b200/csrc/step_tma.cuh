@@ -1,28 +1,35 @@
 // step_tma.cuh — the fused pseudo-time step (K4), TMA-fed and warp-specialised.
 //
-// One persistent CTA per SM: TY consumer warps (a 32 x TY tile of cells per
-// plane, one cell per consumer thread), one TMA issuer warp, one patcher warp.
+// Persistent CTAs (CTAS per SM): TY consumer warps (a 32 x TY tile of cells
+// per plane, one column per consumer thread) and one TMA issuer warp.
 //
-// Issuer (one lane): streams 36 x (TY+4) plane tiles of all five fields (tile
-// plus a 2-cell halo ring) into a ring of R shared-memory slots with
-// cp.async.bulk.tensor.4d (completion = the slot's `full` mbarrier transaction
-// count); it only waits for a slot to be released (`empty`).
-// Patcher (whole warp): as each plane lands it finalises it in place — the
-// lazy rescale fl(p - pc) on interior pressure, and the wall ghosts of
-// apply_boundary_conditions (src/solver.cpp:158-191) for x/y walls — and
-// arrives on the slot's `ready` mbarrier. So consumers read final values only.
+// Issuer (one lane): streams each plane tile into a ring of R shared-memory
+// slots with two cp.async.bulk.tensor.4d boxes — p as 36 x (TY+4) (2-cell
+// halo ring) and u,v,w,T as 4 x 36 x (TY+2) (1-cell y ring), i.e. only the
+// halo each variable's stencil reads (completion = the slot's `full` mbarrier
+// transaction count); it only waits for a slot to be released (`empty`). An
+// optional second cursor prefetches planes ahead into L2.
 //
-// Consumer warps: keep their column's k-window in registers (p: k-2..k+2,
-// u,v,w,T: k-1..k+1; z-wall ghosts are formed there), read in-plane
-// neighbours from the ready slot of plane k, compute residual_t (cell.cuh,
-// the reference's arithmetic), the Euler update, the next step's CFL maxima
-// and the non-finite flags, store, and release the slot (`empty` mbarrier).
-// There is no CTA-wide barrier per plane.
+// Consumer warps wait on `full` directly and never write the ring: the x/y
+// wall ghosts of apply_boundary_conditions (src/solver.cpp:158-191) are formed
+// in registers by the warps whose cells touch a wall (the same
+// apply_wall_ghosts the pointwise kernels use), like the z-wall ghosts in the
+// k-window. Only a pending lazy rescale fl(p - pc) (multi-rank blocks) is
+// patched in place, by all consumer threads, then a consumer-only named
+// barrier. (Measured: a dedicated patcher warp, or cooperative smem wall
+// patches with a barrier per plane, cost 25% of the step on 256^3.)
 //
-// Work: items are (k-chunk, tile) in chunk-major order; CTA c takes items
-// c, c+G, c+2G, ... so the ~G items in flight at any time are neighbouring
-// tiles of the same chunk: their halo rows are L2 hits, every SM gets the same
-// number of items (+-1), and each item restarts the k-window once.
+// Each consumer keeps its column's k-window in registers (p: k-2..k+3,
+// u,v,w,T: k-1..k+2; z-wall ghosts are formed there), computes two planes per
+// step from the in-plane neighbours in the slots, residual_t (cell.cuh, the
+// reference's arithmetic), the Euler update, the next step's CFL maxima and
+// the non-finite flags, stores, and releases the slots (`empty` mbarrier).
+//
+// Work: items are (k-chunk, tile) in chunk-major order; CTA c starts with item
+// c, then takes the next unclaimed item from a global counter, so the ~G items
+// in flight at any time are neighbouring tiles of the same chunk (their halo
+// rows are L2 hits), slower items (wall tiles) do not unbalance the SMs, and
+// each item restarts the k-window once.
 #pragma once
 
 #include <cuda.h>
@@ -84,26 +91,36 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 
 }  // namespace tma
 
-constexpr int kTmaBW = 36;  // 32 + 2x2 halo
-constexpr int kPrefetch = 8;       // L2 prefetch distance, in plane entries
+// Plane tile of one slot: pressure with its 2-cell halo ring (36 x (TY+4))
+// followed by u, v, w, T with their 1-cell y ring (4 x 36 x (TY+2)). Each part
+// is one TMA box; corners are loaded but never read. The u..T rows also start
+// at i0-2: a TMA box must start 16-byte aligned along x (probe:
+// scripts/micro/tma_probe.cu), so an FP64 box cannot start at the odd i0-1.
+constexpr int kPW = 36;            // 32 + 2x2 halo (p)
+constexpr int kQW = 36;            // same x extent for u, v, w, T
 
 // Tile height TY (= consumer warps), ring depth R and CTAs per SM.
 template <int TY_, int R_, int CTAS_>
 struct TmaCfg {
   static constexpr int TY = TY_, R = R_, CTAS = CTAS_;
-  static constexpr int BH = TY + 4;
-  static constexpr int Field = kTmaBW * BH;  // doubles per field plane
-  static constexpr int Slot = 5 * Field;     // doubles per slot
-  static constexpr int Threads = 32 * (TY + 2);  // consumers + issuer + patcher
+  static constexpr int PH = TY + 4, QH = TY + 2;
+  static constexpr int PField = kPW * PH;     // doubles of the p part
+  static constexpr int QField = kQW * QH;     // doubles per u/v/w/T part
+  static constexpr int Slot = PField + 4 * QField;
+  static constexpr int Threads = 32 * (TY + 1);  // consumers + issuer
+  static constexpr int NC = 32 * TY;              // consumer threads
   static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + 5 * kDigits * 8;
-  static_assert(Field * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
-  static_assert(R >= 5, "ring must hold planes k..k+2 plus prefetch");
+  static_assert(PField * 8 % 128 == 0 && Slot * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
+  static_assert(R >= 5, "ring must hold planes k..k+3 plus one in flight");
 };
 
 struct TmaStepArgs {
   double* out;
   Geo g;
   cav_stencil_params sp;
+  double s2fast;  // beta shortcut threshold (host::beta_fast_s2)
+  unsigned* work;  // dynamic item counter (items >= gridDim.x), reset by the last CTA
+  int eager;      // store fl(p' - sc->pcs) and fold pcs_{n+1} (single rank); see IterScalars
   cav_box box;
   const IterScalars* sc;
   Acc* acc;
@@ -140,154 +157,130 @@ __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long it
   return r;
 }
 
-// Consumer-side star accessor: in-plane neighbours from the ready slot,
-// k-neighbours from the register window.
+// Consumer-side star accessor: in-plane neighbours from the landed slot (P at
+// the own pressure cell, U at the own cell of the u part; v, w, T follow at
+// multiples of QF), k-neighbours from the register window. With W, the values
+// of cells next to an x or y wall that lie in the ghost layers are the wall
+// ghosts of apply_boundary_conditions (src/solver.cpp:158-191), formed in
+// registers with exactly device.cuh's apply_wall_ghosts expressions: p by
+// cubic extrapolation, u,v,w antisymmetric, T isothermal 2*t_wall - T on x
+// walls and mirrored on y walls. Nothing is written to the ring.
+constexpr int kXlo2 = 1, kXlo3 = 2, kXhi1 = 4, kXhi0 = 8;       // i == 2, 3, nx+1, nx
+constexpr int kYlo2 = 16, kYlo3 = 32, kYhi1 = 64, kYhi0 = 128;  // j == 2, 3, ny+1, ny
+
+template <int QF, bool W>
 struct SmemAcc {
-  const double *P, *U, *V, *W, *T;
+  const double *P, *U;
   double pc_, pzm_, pzp_, pzm2_, pzp2_;
   double u_, uzm_, uzp_, v_, vzm_, vzp_, w_, wzm_, wzp_, t_, tzm_, tzp_;
+  int fl;
+  double thot, tcold;
+  __device__ __forceinline__ bool on(int bit) const { return W && (fl & bit); }
   __device__ __forceinline__ double p() const { return pc_; }
-  __device__ __forceinline__ double pxm() const { return P[-1]; }
-  __device__ __forceinline__ double pxp() const { return P[1]; }
-  __device__ __forceinline__ double pxm2() const { return P[-2]; }
-  __device__ __forceinline__ double pxp2() const { return P[2]; }
-  __device__ __forceinline__ double pym() const { return P[-kTmaBW]; }
-  __device__ __forceinline__ double pyp() const { return P[kTmaBW]; }
-  __device__ __forceinline__ double pym2() const { return P[-2 * kTmaBW]; }
-  __device__ __forceinline__ double pyp2() const { return P[2 * kTmaBW]; }
+  // stencil row along one axis (stride S): m2 m1 [p] p1 p2
+  template <int S, int LO2, int LO3, int HI1, int HI0>
+  __device__ __forceinline__ double m1() const {
+    if (on(LO2)) return cubic_g0(pc_, P[S], P[2 * S]);
+    return P[-S];
+  }
+  template <int S, int LO2, int LO3, int HI1, int HI0>
+  __device__ __forceinline__ double p1() const {
+    if (on(HI1)) return cubic_g0(pc_, P[-S], P[-2 * S]);
+    return P[S];
+  }
+  template <int S, int LO2, int LO3, int HI1, int HI0>
+  __device__ __forceinline__ double m2() const {
+    if (on(LO2)) return cubic_g1(cubic_g0(pc_, P[S], P[2 * S]), pc_, P[S]);
+    if (on(LO3)) return cubic_g0(P[-S], pc_, P[S]);
+    return P[-2 * S];
+  }
+  template <int S, int LO2, int LO3, int HI1, int HI0>
+  __device__ __forceinline__ double p2() const {
+    if (on(HI1)) return cubic_g1(cubic_g0(pc_, P[-S], P[-2 * S]), pc_, P[-S]);
+    if (on(HI0)) return cubic_g0(P[S], pc_, P[-S]);
+    return P[2 * S];
+  }
+  __device__ __forceinline__ double pxm() const { return m1<1, kXlo2, kXlo3, kXhi1, kXhi0>(); }
+  __device__ __forceinline__ double pxp() const { return p1<1, kXlo2, kXlo3, kXhi1, kXhi0>(); }
+  __device__ __forceinline__ double pxm2() const { return m2<1, kXlo2, kXlo3, kXhi1, kXhi0>(); }
+  __device__ __forceinline__ double pxp2() const { return p2<1, kXlo2, kXlo3, kXhi1, kXhi0>(); }
+  __device__ __forceinline__ double pym() const { return m1<kPW, kYlo2, kYlo3, kYhi1, kYhi0>(); }
+  __device__ __forceinline__ double pyp() const { return p1<kPW, kYlo2, kYlo3, kYhi1, kYhi0>(); }
+  __device__ __forceinline__ double pym2() const { return m2<kPW, kYlo2, kYlo3, kYhi1, kYhi0>(); }
+  __device__ __forceinline__ double pyp2() const { return p2<kPW, kYlo2, kYlo3, kYhi1, kYhi0>(); }
   __device__ __forceinline__ double pzm() const { return pzm_; }
   __device__ __forceinline__ double pzp() const { return pzp_; }
   __device__ __forceinline__ double pzm2() const { return pzm2_; }
   __device__ __forceinline__ double pzp2() const { return pzp2_; }
-#define CAV_Q(F, A)                                                                       \
+  // velocity ghosts (antisymmetric on every wall)
+#define CAV_Q(F, N)                                                                       \
   __device__ __forceinline__ double F() const { return F##_; }                           \
-  __device__ __forceinline__ double F##xm() const { return A[-1]; }                      \
-  __device__ __forceinline__ double F##xp() const { return A[1]; }                       \
-  __device__ __forceinline__ double F##ym() const { return A[-kTmaBW]; }                 \
-  __device__ __forceinline__ double F##yp() const { return A[kTmaBW]; }                  \
+  __device__ __forceinline__ double F##xm() const { return on(kXlo2) ? -F##_ : U[N * QF - 1]; }      \
+  __device__ __forceinline__ double F##xp() const { return on(kXhi1) ? -F##_ : U[N * QF + 1]; }      \
+  __device__ __forceinline__ double F##ym() const { return on(kYlo2) ? -F##_ : U[N * QF - kQW]; }    \
+  __device__ __forceinline__ double F##yp() const { return on(kYhi1) ? -F##_ : U[N * QF + kQW]; }    \
   __device__ __forceinline__ double F##zm() const { return F##zm_; }                     \
   __device__ __forceinline__ double F##zp() const { return F##zp_; }
-  CAV_Q(u, U)
-  CAV_Q(v, V)
-  CAV_Q(w, W)
-  CAV_Q(t, T)
+  CAV_Q(u, 0)
+  CAV_Q(v, 1)
+  CAV_Q(w, 2)
 #undef CAV_Q
+  // temperature: isothermal x walls, adiabatic (mirror) y walls
+  __device__ __forceinline__ double t() const { return t_; }
+  __device__ __forceinline__ double txm() const { return on(kXlo2) ? 2.0 * thot - t_ : U[3 * QF - 1]; }
+  __device__ __forceinline__ double txp() const { return on(kXhi1) ? 2.0 * tcold - t_ : U[3 * QF + 1]; }
+  __device__ __forceinline__ double tym() const { return on(kYlo2) ? t_ : U[3 * QF - kQW]; }
+  __device__ __forceinline__ double typ() const { return on(kYhi1) ? t_ : U[3 * QF + kQW]; }
+  __device__ __forceinline__ double tzm() const { return tzm_; }
+  __device__ __forceinline__ double tzp() const { return tzp_; }
 };
 
-// Producer: finalise one landed plane tile in shared memory (all 32 lanes).
-template <int BH>
-__device__ __forceinline__ void patch_plane(double* slot, const TmaStepArgs& a, const ItemGeom& it, int pl,
-                                            double pc, int lane) {
-  constexpr int kTmaBH = BH, kTmaField = kTmaBW * BH;
+// In-place lazy rescale fl(p - pc) of the interior pressure of a landed plane
+// tile (rescale_pressure, src/solver.cpp:248-257) by all NC consumer threads
+// (t = consumer thread index).
+template <class Cfg>
+__device__ __forceinline__ void coop_rescale(double* P, const TmaStepArgs& a, const ItemGeom& it, double pc, int t) {
+  constexpr int PAIRS = kPW / 2, N = Cfg::PH * PAIRS;
   const Geo& g = a.g;
-  if (pl < 2 || pl >= g.nz + 2) return;  // ghost planes: read only as column values
-  double* P = slot;
   const int i0 = it.ti0 - 2, j0 = it.tj0 - 2;
-  // lazy rescale of interior pressure (rescale_pressure, src/solver.cpp:248-257),
-  // two doubles per lane access; element (x, y) is cell (i0 + x, j0 + y)
-  {
-    constexpr int PAIRS = kTmaBW / 2;
-    int row = lane / PAIRS, c = lane % PAIRS;
-    for (int idx = lane; idx < kTmaBH * PAIRS; idx += 32) {
-      const int j = j0 + row, i = i0 + 2 * c;
-      if (j >= 2 && j < g.ny + 2) {
-        double2* q = reinterpret_cast<double2*>(P + row * kTmaBW + 2 * c);
-        double2 v = *q;
-        if (i >= 2 && i < g.nx + 2) v.x = v.x - pc;
-        if (i + 1 >= 2 && i + 1 < g.nx + 2) v.y = v.y - pc;
-        *q = v;
-      }
-      c += 32 - PAIRS;  // idx += 32 in (row, c) coordinates
-      row += 1;
-      if (c >= PAIRS) {
-        c -= PAIRS;
-        row += 1;
-      }
-    }
-  }
-  __syncwarp();
-  const WallInfo& w = a.walls;
-  double* U = slot + kTmaField;
-  double* V = U + kTmaField;
-  double* W = V + kTmaField;
-  double* T = W + kTmaField;
-  // x walls: ghost columns for rows with interior j
-  if (w.wall[0] && i0 == 0) {
-    for (int y = lane; y < kTmaBH; y += 32) {
-      const int j = j0 + y;
-      if (j < 2 || j >= g.ny + 2) continue;
-      const int r = y * kTmaBW;
-      const double g0 = cubic_g0(P[r + 2], P[r + 3], P[r + 4]);
-      P[r + 1] = g0;
-      P[r] = cubic_g1(g0, P[r + 2], P[r + 3]);
-      U[r + 1] = -U[r + 2];
-      V[r + 1] = -V[r + 2];
-      W[r + 1] = -W[r + 2];
-      T[r + 1] = 2.0 * w.t_hot - T[r + 2];
-    }
-  }
-  const int xg = g.nx + 2 - i0;  // tile column of the high x ghost g0
-  if (w.wall[1] && xg >= 3 && xg < kTmaBW) {
-    for (int y = lane; y < kTmaBH; y += 32) {
-      const int j = j0 + y;
-      if (j < 2 || j >= g.ny + 2) continue;
-      const int r = y * kTmaBW;
-      const double g0 = cubic_g0(P[r + xg - 1], P[r + xg - 2], P[r + xg - 3]);
-      P[r + xg] = g0;
-      if (xg + 1 < kTmaBW) P[r + xg + 1] = cubic_g1(g0, P[r + xg - 1], P[r + xg - 2]);
-      U[r + xg] = -U[r + xg - 1];
-      V[r + xg] = -V[r + xg - 1];
-      W[r + xg] = -W[r + xg - 1];
-      T[r + xg] = 2.0 * w.t_cold - T[r + xg - 1];
-    }
-  }
-  // y walls: ghost rows for columns with interior i
-  if (w.wall[2] && j0 == 0) {
-    for (int x = lane; x < kTmaBW; x += 32) {
-      const int i = i0 + x;
-      if (i < 2 || i >= g.nx + 2) continue;
-      const double g0 = cubic_g0(P[2 * kTmaBW + x], P[3 * kTmaBW + x], P[4 * kTmaBW + x]);
-      P[kTmaBW + x] = g0;
-      P[x] = cubic_g1(g0, P[2 * kTmaBW + x], P[3 * kTmaBW + x]);
-      U[kTmaBW + x] = -U[2 * kTmaBW + x];
-      V[kTmaBW + x] = -V[2 * kTmaBW + x];
-      W[kTmaBW + x] = -W[2 * kTmaBW + x];
-      T[kTmaBW + x] = T[2 * kTmaBW + x];
-    }
-  }
-  const int yg = g.ny + 2 - j0;
-  if (w.wall[3] && yg >= 3 && yg < kTmaBH) {
-    for (int x = lane; x < kTmaBW; x += 32) {
-      const int i = i0 + x;
-      if (i < 2 || i >= g.nx + 2) continue;
-      const double g0 = cubic_g0(P[(yg - 1) * kTmaBW + x], P[(yg - 2) * kTmaBW + x], P[(yg - 3) * kTmaBW + x]);
-      P[yg * kTmaBW + x] = g0;
-      if (yg + 1 < kTmaBH) P[(yg + 1) * kTmaBW + x] = cubic_g1(g0, P[(yg - 1) * kTmaBW + x], P[(yg - 2) * kTmaBW + x]);
-      U[yg * kTmaBW + x] = -U[(yg - 1) * kTmaBW + x];
-      V[yg * kTmaBW + x] = -V[(yg - 1) * kTmaBW + x];
-      W[yg * kTmaBW + x] = -W[(yg - 1) * kTmaBW + x];
-      T[yg * kTmaBW + x] = T[(yg - 1) * kTmaBW + x];
+  for (int idx = t; idx < N; idx += Cfg::NC) {
+    const int row = idx / PAIRS, c = idx - row * PAIRS;
+    const int j = j0 + row, i = i0 + 2 * c;
+    if (j >= 2 && j < g.ny + 2) {
+      double2* q = reinterpret_cast<double2*>(P + row * kPW + 2 * c);
+      double2 v = *q;
+      if (i >= 2 && i < g.nx + 2) v.x = v.x - pc;
+      if (i + 1 >= 2 && i + 1 < g.nx + 2) v.y = v.y - pc;
+      *q = v;
     }
   }
 }
 
+// Whether plane `pl` of item `it` needs the lazy rescale before use: a shift
+// is pending (multi-rank blocks) and its bit pattern is not +0.0 (subtracting
+// +0.0 is the identity; subtracting -0.0 is not). Uniform across the CTA's
+// consumer warps, so the named barrier it implies is too.
+__device__ __forceinline__ bool plane_needs_rescale(const TmaStepArgs& a, int pl, bool lazy) {
+  return lazy && pl >= 2 && pl < a.g.nz + 2;  // ghost planes are read only as column values
+}
+
 template <class Cfg, bool NORMS>
 __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
-    k_step_tma(const __grid_constant__ CUtensorMap map, const TmaStepArgs a) {
-  constexpr int C = Cfg::TY, R = Cfg::R, BW = kTmaBW;
-  constexpr int kTmaField = Cfg::Field, kTmaSlot = Cfg::Slot, kTmaThreads = Cfg::Threads;
+    k_step_tma(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
+               const TmaStepArgs a) {
+  constexpr int C = Cfg::TY, R = Cfg::R;
+  constexpr int kTmaSlot = Cfg::Slot, kTmaThreads = Cfg::Threads, QF = Cfg::QField;
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + R * kTmaSlot * sizeof(double));
-  uint64_t* ready = full + R;
-  uint64_t* empty = ready + R;
-  unsigned long long* sdig = reinterpret_cast<unsigned long long*>(empty + R);
+  uint64_t* empty = full + R;
+  long long* sitem = reinterpret_cast<long long*>(empty + R);  // item of each slot's entry (-1 = end)
+  unsigned long long* sdig = reinterpret_cast<unsigned long long*>(sitem + R);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {
       tma::mbar_init(&full[s], 1);
-      tma::mbar_init(&ready[s], 1);
       tma::mbar_init(&empty[s], C);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -299,74 +292,44 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
   const long long G = gridDim.x;
   const double pc = a.sc->pc;
+  const bool lazy = __double_as_longlong(pc) != 0;
 
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
-    // A second cursor runs kPrefetch entries ahead and pulls those planes
-    // into L2 (no smem), so the ring's own loads hit L2 instead of waiting
-    // out DRAM latency with only R-3 slots in flight.
     if (lane != 0) return;
     int s = 0;
     uint32_t ph = 0, e = 0;  // slot / empty-barrier phase of entry e
-    long long pf_item = blockIdx.x;
-    ItemGeom pf{0, 0, 0, 0};
-    int pf_pl = 0;
-    if (pf_item < total) {
-      pf = item_geom<C>(a, pf_item);
-      pf_pl = pf.kb - 2;
-    }
-    auto prefetch_next = [&]() {
-      if (pf_item >= total) return;
-#pragma unroll
-      for (int f = 0; f < 5; ++f) tma::prefetch_4d(&map, a.g.off + pf.ti0 - 2, pf.tj0 - 2, pf_pl, f);
-      if (++pf_pl > pf.ke + 1) {
-        pf_item += G;
-        if (pf_item < total) {
-          pf = item_geom<C>(a, pf_item);
-          pf_pl = pf.kb - 2;
-        }
-      }
-    };
-    for (int q = 0; q < kPrefetch; ++q) prefetch_next();
-    for (long long item = blockIdx.x; item < total; item += G) {
-      const ItemGeom it = item_geom<C>(a, item);
+    // Items: blockIdx.x first, then dynamically from a.work (wall tiles and
+    // the odd item out make static round-robin uneven). Each entry's item is
+    // written to sitem[] before the slot's arrive, which releases it to the
+    // consumers' acquire on `full`.
+    long long item = blockIdx.x;
+    for (;;) {
+      const bool done = item >= total;
+      const ItemGeom it = item_geom<C>(a, done ? 0 : item);
       const int x0 = a.g.off + it.ti0 - 2, y0 = it.tj0 - 2;
-      for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl, ++e) {
-        prefetch_next();
+      const int pe = done ? it.kb - 2 : it.ke + 1;  // one sentinel entry after the last item
+      for (int pl = it.kb - 2; pl <= pe; ++pl, ++e) {
         if (e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[s], ph ^ 1);
-        tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
-        double* dst = ring + s * kTmaSlot;
-#pragma unroll
-        for (int f = 0; f < 5; ++f) tma::load_4d(dst + f * kTmaField, &map, x0, y0, pl, f, &full[s]);
+        sitem[s] = done ? -1 : item;
+        if (done) {
+          tma::mbar_arrive(&full[s]);
+        } else {
+          tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
+          double* dst = ring + s * kTmaSlot;
+          tma::load_4d(dst, &mapP, x0, y0, pl, 0, &full[s]);
+          tma::load_4d(dst + Cfg::PField, &mapQ, x0, y0 + 1, pl, 0, &full[s]);
+        }
         if (++s == R) {
           s = 0;
           ph ^= 1;
         }
       }
+      if (done) break;
+      item = G + atomicAdd(a.work, 1u);
     }
     return;
   }
-  if (warp == C + 1) {
-    // ---------------- patcher (whole warp) ----------------
-    int s = 0;
-    uint32_t ph = 0;
-    for (long long item = blockIdx.x; item < total; item += G) {
-      const ItemGeom it = item_geom<C>(a, item);
-      for (int pl = it.kb - 2; pl <= it.ke + 1; ++pl) {
-        tma::mbar_wait(&full[s], ph);
-        patch_plane<Cfg::BH>(ring + s * kTmaSlot, a, it, pl, pc, lane);
-        tma::fence_proxy_async();  // generic writes before the slot's next TMA fill
-        __syncwarp();
-        if (lane == 0) tma::mbar_arrive(&ready[s]);
-        if (++s == R) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    return;
-  }
-
   // ---------------- consumers ----------------
   // Each step computes two planes (k, k+1) of the thread's column: the
   // k-windows are shared (p: k-2..k+3, u,v,w,T: k-1..k+2), waits/releases and
@@ -374,14 +337,15 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // residuals interleave.
   const int tx = lane, ty = warp;
   const Geo g = a.g;
-  const double dt = a.sc->dt, u_ref = a.sp.u_ref;
+  const double dt = a.sc->dt, u_ref = a.sp.u_ref, s2fast = a.s2fast, pcs = a.sc->pcs;
   const long long fs = g.fstride;
   const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
   const bool zlo = a.walls.wall[4], zhi = a.walls.wall[5];
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
-  const double* ringc = ring + (ty + 2) * BW + tx + 2;  // own cell in slot 0, field 0
+  const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
+  const double* ringq = ring + Cfg::PField + (ty + 1) * kQW + tx + 2;  // own u cell in slot 0
   int sw = 0;  // slot of the next entry to wait for, and its phase
   uint32_t phw = 0;
   auto advance = [&](int& sl, uint32_t& ph) {
@@ -390,17 +354,34 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       ph ^= 1;
     }
   };
-  auto wait_next = [&]() {
-    const int sl = sw;
-    tma::mbar_wait(&ready[sw], phw);
-    advance(sw, phw);
-    return sl;
+  // Wait for the planes of one step (1 or 2 consecutive entries) to land, then
+  // finalise the ones that need it: all consumer threads patch, a named
+  // barrier per phase makes the patches visible to every consumer warp, and
+  // the writers' proxy fence orders them before the slot's next TMA fill.
+  const int tid = threadIdx.x;
+  int wfl = 0;        // wall flags of this thread's column (kXlo2 ... kYhi0)
+  bool wwarp = false;  // some lane of this warp has a wall flag (warp-uniform)
+  auto wait_planes = [&](const ItemGeom& it, int pl, int count, int* sl) {
+    bool any = false;
+    for (int q = 0; q < count; ++q) {
+      sl[q] = sw;
+      tma::mbar_wait(&full[sw], phw);
+      advance(sw, phw);
+      any = any || plane_needs_rescale(a, pl + q, lazy);
+    }
+    if (any) {
+      for (int q = 0; q < count; ++q)
+        if (plane_needs_rescale(a, pl + q, lazy)) coop_rescale<Cfg>(ring + sl[q] * kTmaSlot, a, it, pc, tid);
+      tma::named_sync(1, Cfg::NC);
+    }
+    if (any) tma::fence_proxy_async();
   };
   auto release_slot = [&](int sl) {
     __syncwarp();
     if (lane == 0) tma::mbar_arrive(&empty[sl]);
   };
   auto slot = [&](int sl) { return ringc + sl * kTmaSlot; };
+  auto qslot = [&](int sl) { return ringq + sl * kTmaSlot; };
 
   // z-wall ghosts inside the register windows (apply_boundary_conditions for
   // the z walls). Two-plane step at k: P[0..5] = planes k-2..k+3,
@@ -446,13 +427,19 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   };
 
   // one cell: residual + update + store + bookkeeping
-  auto cell = [&](const double* B, double p0, double pzm, double pzp, double pzm2, double pzp2, const double* qc,
+  auto cell = [&](int sl, double p0, double pzm, double pzp, double pzm2, double pzp2, const double* qc,
                   const double* qm, const double* qp, double* op, bool ccolk) {
-    const SmemAcc sa{B, B + kTmaField, B + 2 * kTmaField, B + 3 * kTmaField, B + 4 * kTmaField,
-                     p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1], qp[1], qc[2], qm[2], qp[2],
-                     qc[3], qm[3], qp[3]};
-    const Res r = residual_t(sa, a.sp);
-    const double qpn = p0 + dt * r.p, qun = qc[0] + dt * r.u, qvn = qc[1] + dt * r.v, qwn = qc[2] + dt * r.w,
+    Res r;
+    if (wwarp) {  // warp-uniform: a lane of this warp is next to an x or y wall
+      const SmemAcc<QF, true> sa{slot(sl), qslot(sl), p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1], qp[1],
+                                 qc[2], qm[2], qp[2], qc[3], qm[3], qp[3], wfl, a.walls.t_hot, a.walls.t_cold};
+      r = residual_t(sa, a.sp, s2fast);
+    } else {
+      const SmemAcc<QF, false> sa{slot(sl), qslot(sl), p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1],
+                                  qp[1], qc[2], qm[2], qp[2], qc[3], qm[3], qp[3], 0, 0.0, 0.0};
+      r = residual_t(sa, a.sp, s2fast);
+    }
+    const double qpp = p0 + dt * r.p, qpn = qpp - pcs, qun = qc[0] + dt * r.u, qvn = qc[1] + dt * r.v, qwn = qc[2] + dt * r.w,
                  qtn = qc[3] + dt * r.t;
     // explicit global (streaming) stores: no possible aliasing with the
     // shared-memory ring, so the two cells of a step can interleave
@@ -461,7 +448,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     __stcs(op + 2 * fs, qvn);
     __stcs(op + 3 * fs, qwn);
     __stcs(op + 4 * fs, qtn);
-    const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref);
+    const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, s2fast);
     m0 = dmax_d(m0, d.du);
     m1 = dmax_d(m1, d.dv);
     m2 = dmax_d(m2, d.dw);
@@ -470,7 +457,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     e_v = max(e_v, static_cast<unsigned>(__double2hiint(qvn)) & 0x7FF00000u);
     e_w = max(e_w, static_cast<unsigned>(__double2hiint(qwn)) & 0x7FF00000u);
     e_t = max(e_t, static_cast<unsigned>(__double2hiint(qtn)) & 0x7FF00000u);
-    if (ccolk) a.acc->pc_local = qpn;
+    if (ccolk) a.acc->pc_local = qpp;
     if (NORMS) {
       const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
 #pragma unroll
@@ -481,14 +468,30 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
   };
 
-  for (long long item = blockIdx.x; item < total; item += G) {
+  for (;;) {
+    tma::mbar_wait(&full[sw], phw);  // the next entry's item (re-waited below: completed phase)
+    const long long item = sitem[sw];
+    if (item < 0) break;
     const ItemGeom it = item_geom<C>(a, item);
     const int len = it.ke - it.kb;
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
     const bool ccol = i == a.cx && j == a.cy;
+    // x/y walls next to this thread's column: register ghosts (SmemAcc<.., true>)
+    {
+      const WallInfo& w = a.walls;
+      wfl = (w.wall[0] && i == 2 ? kXlo2 : 0) | (w.wall[0] && i == 3 ? kXlo3 : 0) |
+            (w.wall[1] && i == g.nx + 1 ? kXhi1 : 0) | (w.wall[1] && i == g.nx ? kXhi0 : 0) |
+            (w.wall[2] && j == 2 ? kYlo2 : 0) | (w.wall[2] && j == 3 ? kYlo3 : 0) |
+            (w.wall[3] && j == g.ny + 1 ? kYhi1 : 0) | (w.wall[3] && j == g.ny ? kYhi0 : 0);
+      if (!active) wfl = 0;
+      wwarp = __any_sync(0xffffffffu, wfl != 0);
+    }
     // prologue: planes kb-2 .. kb+1
-    const int s0 = wait_next(), s1 = wait_next(), s2 = wait_next(), s3 = wait_next();
+    int sa[2], sb[2];
+    wait_planes(it, it.kb - 2, 2, sa);
+    wait_planes(it, it.kb, 2, sb);
+    const int s0 = sa[0], s1 = sa[1], s2 = sb[0], s3 = sb[1];
     double P[6];     // p at planes k-2 .. k+3
     double Q[4][4];  // u,v,w,T at planes k-1 .. k+2
     P[0] = slot(s0)[0];
@@ -497,8 +500,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     P[3] = slot(s3)[0];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
-      Q[f][0] = slot(s1)[(f + 1) * kTmaField];
-      Q[f][1] = slot(s2)[(f + 1) * kTmaField];
+      Q[f][0] = qslot(s1)[f * QF];
+      Q[f][1] = qslot(s2)[f * QF];
     }
     release_slot(s0);
     release_slot(s1);
@@ -507,13 +510,15 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     int st = 0;
     for (; st + 1 < len; st += 2, op += 2 * plane) {
       const int k = it.kb + st;
-      const int sc2 = wait_next(), sc3 = wait_next();  // planes k+2, k+3
+      int sn[2];
+      wait_planes(it, k + 2, 2, sn);  // planes k+2, k+3
+      const int sc2 = sn[0], sc3 = sn[1];
       P[4] = slot(sc2)[0];
       P[5] = slot(sc3)[0];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
-        Q[f][2] = slot(sc1)[(f + 1) * kTmaField];
-        Q[f][3] = slot(sc2)[(f + 1) * kTmaField];
+        Q[f][2] = qslot(sc1)[f * QF];
+        Q[f][3] = qslot(sc2)[f * QF];
       }
       if ((zlo && k <= 3) || (zhi && k + 3 >= g.nz + 2)) zwall2(P, Q, k);
       if (active) {
@@ -521,8 +526,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
         const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
         const double qbp[4] = {Q[0][3], Q[1][3], Q[2][3], Q[3][3]};
-        cell(slot(sc0), P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
-        cell(slot(sc1), P[3], P[2], P[4], P[1], P[5], qap, qa, qbp, op + plane, ccol && k + 1 == a.cz);
+        cell(sc0, P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
+        cell(sc1, P[3], P[2], P[4], P[1], P[5], qap, qa, qbp, op + plane, ccol && k + 1 == a.cz);
       }
       release_slot(sc0);
       release_slot(sc1);
@@ -540,16 +545,18 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
     if (st < len) {  // odd remainder: one plane
       const int k = it.kb + st;
-      const int sc2 = wait_next();  // plane k+2
+      int sn[2];
+      wait_planes(it, k + 2, 1, sn);  // plane k+2
+      const int sc2 = sn[0];
       P[4] = slot(sc2)[0];
 #pragma unroll
-      for (int f = 0; f < 4; ++f) Q[f][2] = slot(sc1)[(f + 1) * kTmaField];
+      for (int f = 0; f < 4; ++f) Q[f][2] = qslot(sc1)[f * QF];
       if ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2)) zwall1(P, Q, k);
       if (active) {
         const double qa[4] = {Q[0][1], Q[1][1], Q[2][1], Q[3][1]};
         const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
         const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
-        cell(slot(sc0), P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
+        cell(sc0, P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
       }
       release_slot(sc0);
       sc0 = sc1;
@@ -595,24 +602,35 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
     acc_publish(a.acc, m0, m1, m2, mk & 0xFF, a.n + 1, a.rank);
     if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
-    if (a.fold) {
+    __threadfence();
+    if (atomicAdd(a.done, 1u) == gridDim.x - 1) {  // every CTA has published
+      *a.work = 0;
       __threadfence();
-      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {  // every CTA has published
-        __threadfence();
+      if (a.fold) {
         volatile Acc* acc = a.acc;
         const unsigned long long dm[3] = {acc->dmax[0], acc->dmax[1], acc->dmax[2]};
         cav_fluid_params fl{};
         fl.nu = a.nu;
         fl.alpha = a.alpha;
-        a.sc_next->dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, fl, a.cfl);
-        a.sc_next->pc = a.rescale ? acc->pc_local : 0.0;
+        const double dtn = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, fl, a.cfl);
+        a.sc_next->dt = dtn;
+        if (a.eager) {
+          // this iteration's output is final; pcs_{n+1} = p'(centre) of the
+          // next step, from the same inputs and arithmetic as that step
+          a.sc_next->pc = 0.0;
+          a.sc_next->pcs = a.rescale ? center_p_update(a.out, a.g, a.walls, a.sp, a.s2fast, dtn, 0.0, a.cx,
+                                                       a.cy, a.cz)
+                                     : 0.0;
+        } else {
+          a.sc_next->pc = a.rescale ? acc->pc_local : 0.0;
+        }
         const unsigned long long e = acc->err;
         if (e < *a.err_sticky) *a.err_sticky = e;
         Acc z{};
         z.err = ~0ull;
         *a.acc_next = z;
-        *a.done = 0;
       }
+      *a.done = 0;
     }
   }
   if (NORMS)
