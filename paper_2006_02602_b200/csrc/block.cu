@@ -724,8 +724,8 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw
 
 // TMA step variants (tile height, ring depth, CTAs per SM); CAV_TMA_CFG picks
 // one for experiments, variant 0 is the default.
-using TmaV0 = TmaCfg<12, 10, 1>;  // default: 13 warps -> 128 registers, 6 slots in flight
-using TmaV1 = TmaCfg<8, 7, 2>;
+using TmaV0 = TmaCfg<8, 7, 2>;  // default: 2 CTAs x (8 consumer + 1 issuer warps) per SM
+using TmaV1 = TmaCfg<12, 10, 1>;
 using TmaV2 = TmaCfg<8, 14, 1>;
 using TmaV3 = TmaCfg<16, 8, 1>;
 constexpr int kTmaVariants = 4;

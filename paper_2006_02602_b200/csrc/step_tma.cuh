@@ -19,9 +19,10 @@
 // barrier. (Measured: a dedicated patcher warp, or cooperative smem wall
 // patches with a barrier per plane, cost 25% of the step on 256^3.)
 //
-// Each consumer keeps its column's k-window in registers (p: k-2..k+3,
-// u,v,w,T: k-1..k+2; z-wall ghosts are formed there), computes two planes per
-// step from the in-plane neighbours in the slots, residual_t (cell.cuh, the
+// Each consumer keeps its column's p k-window in registers (k-2..k+3; z-wall
+// ghosts are formed there) and reads u,v,w,T at k-1..k+1 from the slots it
+// holds (planes k-1..k+3, five slots), computes two planes per step,
+// residual_t (cell.cuh, the
 // reference's arithmetic), the Euler update, the next step's CFL maxima and
 // the non-finite flags, stores, and releases the slots (`empty` mbarrier).
 //
@@ -68,6 +69,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(1000000u)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t r;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(r)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return r != 0;
 }
 __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int x, int y, int z, int f,
                                         uint64_t* bar) {
@@ -157,9 +171,10 @@ __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long it
   return r;
 }
 
-// Consumer-side star accessor: in-plane neighbours from the landed slot (P at
-// the own pressure cell, U at the own cell of the u part; v, w, T follow at
-// multiples of QF), k-neighbours from the register window. With W, the values
+// Consumer-side star accessor: p's in-plane neighbours from the landed slot
+// of plane k, its k-neighbours from the register window; u, v, w, T entirely
+// from the slots of planes k-1, k, k+1 (v, w, T follow u at multiples of QF).
+// With W, the values
 // of cells next to an x or y wall that lie in the ghost layers are the wall
 // ghosts of apply_boundary_conditions (src/solver.cpp:158-191), formed in
 // registers with exactly device.cuh's apply_wall_ghosts expressions: p by
@@ -167,15 +182,18 @@ __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long it
 // walls and mirrored on y walls. Nothing is written to the ring.
 constexpr int kXlo2 = 1, kXlo3 = 2, kXhi1 = 4, kXhi0 = 8;       // i == 2, 3, nx+1, nx
 constexpr int kYlo2 = 16, kYlo3 = 32, kYhi1 = 64, kYhi0 = 128;  // j == 2, 3, ny+1, ny
+constexpr int kZlo2 = 256, kZhi1 = 512;                         // k == 2, nz+1 (u,v,w,T only)
 
-template <int QF, bool W>
+template <int QF, bool WX, bool WYZ>
 struct SmemAcc {
-  const double *P, *U;
+  const double *P, *Um, *U, *Up;  // own cell: p in slot k; u part in slots k-1, k, k+1
   double pc_, pzm_, pzp_, pzm2_, pzp2_;
-  double u_, uzm_, uzp_, v_, vzm_, vzp_, w_, wzm_, wzp_, t_, tzm_, tzp_;
   int fl;
   double thot, tcold;
-  __device__ __forceinline__ bool on(int bit) const { return W && (fl & bit); }
+  // WX: x-wall flags may be set; WYZ: y- or z-wall flags may be set
+  __device__ __forceinline__ bool on(int bit) const {
+    return ((bit < kYlo2) ? WX : WYZ) && (fl & bit);
+  }
   __device__ __forceinline__ double p() const { return pc_; }
   // stencil row along one axis (stride S): m2 m1 [p] p1 p2
   template <int S, int LO2, int LO3, int HI1, int HI0>
@@ -213,26 +231,26 @@ struct SmemAcc {
   __device__ __forceinline__ double pzm2() const { return pzm2_; }
   __device__ __forceinline__ double pzp2() const { return pzp2_; }
   // velocity ghosts (antisymmetric on every wall)
-#define CAV_Q(F, N)                                                                       \
-  __device__ __forceinline__ double F() const { return F##_; }                           \
-  __device__ __forceinline__ double F##xm() const { return on(kXlo2) ? -F##_ : U[N * QF - 1]; }      \
-  __device__ __forceinline__ double F##xp() const { return on(kXhi1) ? -F##_ : U[N * QF + 1]; }      \
-  __device__ __forceinline__ double F##ym() const { return on(kYlo2) ? -F##_ : U[N * QF - kQW]; }    \
-  __device__ __forceinline__ double F##yp() const { return on(kYhi1) ? -F##_ : U[N * QF + kQW]; }    \
-  __device__ __forceinline__ double F##zm() const { return F##zm_; }                     \
-  __device__ __forceinline__ double F##zp() const { return F##zp_; }
+#define CAV_Q(F, N)                                                                                   \
+  __device__ __forceinline__ double F() const { return U[N * QF]; }                                  \
+  __device__ __forceinline__ double F##xm() const { return on(kXlo2) ? -F() : U[N * QF - 1]; }      \
+  __device__ __forceinline__ double F##xp() const { return on(kXhi1) ? -F() : U[N * QF + 1]; }      \
+  __device__ __forceinline__ double F##ym() const { return on(kYlo2) ? -F() : U[N * QF - kQW]; }    \
+  __device__ __forceinline__ double F##yp() const { return on(kYhi1) ? -F() : U[N * QF + kQW]; }    \
+  __device__ __forceinline__ double F##zm() const { return on(kZlo2) ? -F() : Um[N * QF]; }         \
+  __device__ __forceinline__ double F##zp() const { return on(kZhi1) ? -F() : Up[N * QF]; }
   CAV_Q(u, 0)
   CAV_Q(v, 1)
   CAV_Q(w, 2)
 #undef CAV_Q
-  // temperature: isothermal x walls, adiabatic (mirror) y walls
-  __device__ __forceinline__ double t() const { return t_; }
-  __device__ __forceinline__ double txm() const { return on(kXlo2) ? 2.0 * thot - t_ : U[3 * QF - 1]; }
-  __device__ __forceinline__ double txp() const { return on(kXhi1) ? 2.0 * tcold - t_ : U[3 * QF + 1]; }
-  __device__ __forceinline__ double tym() const { return on(kYlo2) ? t_ : U[3 * QF - kQW]; }
-  __device__ __forceinline__ double typ() const { return on(kYhi1) ? t_ : U[3 * QF + kQW]; }
-  __device__ __forceinline__ double tzm() const { return tzm_; }
-  __device__ __forceinline__ double tzp() const { return tzp_; }
+  // temperature: isothermal x walls, adiabatic (mirror) y and z walls
+  __device__ __forceinline__ double t() const { return U[3 * QF]; }
+  __device__ __forceinline__ double txm() const { return on(kXlo2) ? 2.0 * thot - t() : U[3 * QF - 1]; }
+  __device__ __forceinline__ double txp() const { return on(kXhi1) ? 2.0 * tcold - t() : U[3 * QF + 1]; }
+  __device__ __forceinline__ double tym() const { return on(kYlo2) ? t() : U[3 * QF - kQW]; }
+  __device__ __forceinline__ double typ() const { return on(kYhi1) ? t() : U[3 * QF + kQW]; }
+  __device__ __forceinline__ double tzm() const { return on(kZlo2) ? t() : Um[3 * QF]; }
+  __device__ __forceinline__ double tzp() const { return on(kZhi1) ? t() : Up[3 * QF]; }
 };
 
 // In-place lazy rescale fl(p - pc) of the interior pressure of a landed plane
@@ -262,6 +280,63 @@ __device__ __forceinline__ void coop_rescale(double* P, const TmaStepArgs& a, co
 // consumer warps, so the named barrier it implies is too.
 __device__ __forceinline__ bool plane_needs_rescale(const TmaStepArgs& a, int pl, bool lazy) {
   return lazy && pl >= 2 && pl < a.g.nz + 2;  // ghost planes are read only as column values
+}
+
+// TMA issue cursor of the issuer warp (lane 0). (Measured: folding it into
+// consumer warp 0 to free a warp slot was 16% slower — the ring is only fed
+// when that warp reaches a wait.) Items:
+// blockIdx.x first, then dynamically from a.work (wall tiles and the odd
+// item out make a static round-robin uneven). Each entry's item id goes to
+// sitem[] before the slot's arrive, which releases it to the consumers'
+// acquire on `full`; after the last item one sentinel entry (-1) is issued.
+struct Issuer {
+  long long item;
+  ItemGeom it;
+  int pl;
+  int s;
+  uint32_t ph, e;  // slot, its empty-barrier phase, entries issued
+  bool done, fin;
+};
+
+// Issues the next entry if its slot is free (or after waiting for it when
+// `block`); false when nothing was issued.
+template <class Cfg>
+__device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, const CUtensorMap* mQ,
+                                          const TmaStepArgs& a, double* ring, uint64_t* full, uint64_t* empty,
+                                          long long* sitem, long long total, bool block) {
+  constexpr int R = Cfg::R;
+  if (q.fin) return false;
+  if (q.e >= static_cast<uint32_t>(R)) {
+    if (block) tma::mbar_wait(&empty[q.s], q.ph ^ 1);
+    else if (!tma::mbar_test(&empty[q.s], q.ph ^ 1)) return false;
+  }
+  if (q.done) {
+    sitem[q.s] = -1;
+    tma::mbar_arrive(&full[q.s]);
+    q.fin = true;
+  } else {
+    sitem[q.s] = q.item;
+    tma::mbar_expect_tx(&full[q.s], Cfg::Slot * sizeof(double));
+    double* dst = ring + q.s * Cfg::Slot;
+    const int x0 = a.g.off + q.it.ti0 - 2, y0 = q.it.tj0 - 2;
+    tma::load_4d(dst, mP, x0, y0, q.pl, 0, &full[q.s]);
+    tma::load_4d(dst + Cfg::PField, mQ, x0, y0 + 1, q.pl, 0, &full[q.s]);
+    if (++q.pl > q.it.ke + 1) {
+      q.item = gridDim.x + atomicAdd(a.work, 1u);
+      if (q.item >= total) {
+        q.done = true;
+      } else {
+        q.it = item_geom<Cfg::TY>(a, q.item);
+        q.pl = q.it.kb - 2;
+      }
+    }
+  }
+  if (++q.s == R) {
+    q.s = 0;
+    q.ph ^= 1;
+  }
+  ++q.e;
+  return true;
 }
 
 template <class Cfg, bool NORMS>
@@ -297,36 +372,14 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
     if (lane != 0) return;
-    int s = 0;
-    uint32_t ph = 0, e = 0;  // slot / empty-barrier phase of entry e
-    // Items: blockIdx.x first, then dynamically from a.work (wall tiles and
-    // the odd item out make static round-robin uneven). Each entry's item is
-    // written to sitem[] before the slot's arrive, which releases it to the
-    // consumers' acquire on `full`.
-    long long item = blockIdx.x;
-    for (;;) {
-      const bool done = item >= total;
-      const ItemGeom it = item_geom<C>(a, done ? 0 : item);
-      const int x0 = a.g.off + it.ti0 - 2, y0 = it.tj0 - 2;
-      const int pe = done ? it.kb - 2 : it.ke + 1;  // one sentinel entry after the last item
-      for (int pl = it.kb - 2; pl <= pe; ++pl, ++e) {
-        if (e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[s], ph ^ 1);
-        sitem[s] = done ? -1 : item;
-        if (done) {
-          tma::mbar_arrive(&full[s]);
-        } else {
-          tma::mbar_expect_tx(&full[s], kTmaSlot * sizeof(double));
-          double* dst = ring + s * kTmaSlot;
-          tma::load_4d(dst, &mapP, x0, y0, pl, 0, &full[s]);
-          tma::load_4d(dst + Cfg::PField, &mapQ, x0, y0 + 1, pl, 0, &full[s]);
-        }
-        if (++s == R) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
-      if (done) break;
-      item = G + atomicAdd(a.work, 1u);
+    Issuer iq{};
+    iq.item = blockIdx.x;
+    iq.done = iq.item >= total;
+    if (!iq.done) {
+      iq.it = item_geom<C>(a, iq.item);
+      iq.pl = iq.it.kb - 2;
+    }
+    while (issue_one<Cfg>(iq, &mapP, &mapQ, a, ring, full, empty, sitem, total, true)) {
     }
     return;
   }
@@ -359,8 +412,12 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // barrier per phase makes the patches visible to every consumer warp, and
   // the writers' proxy fence orders them before the slot's next TMA fill.
   const int tid = threadIdx.x;
-  int wfl = 0;        // wall flags of this thread's column (kXlo2 ... kYhi0)
-  bool wwarp = false;  // some lane of this warp has a wall flag (warp-uniform)
+  int wfl = 0;         // wall flags of this thread's column (kXlo2 ... kYhi0)
+  bool wx = false, wyz = false;  // some lane of this warp has an x / y wall flag (warp-uniform)
+  // Warp 0 keeps the ring fed: everything whose slot is free now, and at
+  // least through entry `need` (blocking on its slot if necessary; the
+  // entries that slot's holders wait for are all issued, so this cannot
+  // deadlock).
   auto wait_planes = [&](const ItemGeom& it, int pl, int count, int* sl) {
     bool any = false;
     for (int q = 0; q < count; ++q) {
@@ -383,21 +440,14 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   auto slot = [&](int sl) { return ringc + sl * kTmaSlot; };
   auto qslot = [&](int sl) { return ringq + sl * kTmaSlot; };
 
-  // z-wall ghosts inside the register windows (apply_boundary_conditions for
-  // the z walls). Two-plane step at k: P[0..5] = planes k-2..k+3,
-  // Q[f][0..3] = planes k-1..k+2; one-plane step: P[0..4], Q[f][0..2].
-  // Only compile-time indices, so the windows stay in registers.
-  auto qmirror = [&](double (*Q)[4], int gi, int ii) {  // ghost gi from interior ii
-    Q[0][gi] = -Q[0][ii];
-    Q[1][gi] = -Q[1][ii];
-    Q[2][gi] = -Q[2][ii];
-    Q[3][gi] = Q[3][ii];
-  };
-  auto zwall2 = [&](double* P, double (*Q)[4], int k) {
+  // z-wall ghosts of p inside the register window (apply_boundary_conditions
+  // for the z walls; u,v,w,T z ghosts are the accessor's kZlo2/kZhi1).
+  // Two-plane step at k: P[0..5] = planes k-2..k+3; one-plane step: P[0..4].
+  // Only compile-time indices, so the window stays in registers.
+  auto zwall2 = [&](double* P, int k) {
     if (zlo && k == 2) {
       P[1] = cubic_g0(P[2], P[3], P[4]);
       P[0] = cubic_g1(P[1], P[2], P[3]);
-      qmirror(Q, 0, 1);
     } else if (zlo && k == 3) {
       P[0] = cubic_g0(P[1], P[2], P[3]);
     }
@@ -406,14 +456,12 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     } else if (zhi && k == g.nz) {
       P[4] = cubic_g0(P[3], P[2], P[1]);
       P[5] = cubic_g1(P[4], P[3], P[2]);
-      qmirror(Q, 3, 2);
     }
   };
-  auto zwall1 = [&](double* P, double (*Q)[4], int k) {
+  auto zwall1 = [&](double* P, int k) {
     if (zlo && k == 2) {
       P[1] = cubic_g0(P[2], P[3], P[4]);
       P[0] = cubic_g1(P[1], P[2], P[3]);
-      qmirror(Q, 0, 1);
     } else if (zlo && k == 3) {
       P[0] = cubic_g0(P[1], P[2], P[3]);
     }
@@ -422,25 +470,34 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     } else if (zhi && k == g.nz + 1) {
       P[3] = cubic_g0(P[2], P[1], P[0]);
       P[4] = cubic_g1(P[3], P[2], P[1]);
-      qmirror(Q, 2, 1);
     }
   };
 
-  // one cell: residual + update + store + bookkeeping
-  auto cell = [&](int sl, double p0, double pzm, double pzp, double pzm2, double pzp2, const double* qc,
-                  const double* qm, const double* qp, double* op, bool ccolk) {
+  // one cell at plane kk: residual + update + store + bookkeeping. Slots
+  // slm, slk, slp hold planes kk-1, kk, kk+1.
+  auto cell = [&](int slm, int slk, int slp, int kk, double p0, double pzm, double pzp, double pzm2, double pzp2,
+                  double* op, bool ccolk) {
+    const int zf = (zlo && kk == 2 ? kZlo2 : 0) | (zhi && kk == g.nz + 1 ? kZhi1 : 0);
     Res r;
-    if (wwarp) {  // warp-uniform: a lane of this warp is next to an x or y wall
-      const SmemAcc<QF, true> sa{slot(sl), qslot(sl), p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1], qp[1],
-                                 qc[2], qm[2], qp[2], qc[3], qm[3], qp[3], wfl, a.walls.t_hot, a.walls.t_cold};
-      r = residual_t(sa, a.sp, s2fast);
-    } else {
-      const SmemAcc<QF, false> sa{slot(sl), qslot(sl), p0, pzm, pzp, pzm2, pzp2, qc[0], qm[0], qp[0], qc[1], qm[1],
-                                  qp[1], qc[2], qm[2], qp[2], qc[3], qm[3], qp[3], 0, 0.0, 0.0};
-      r = residual_t(sa, a.sp, s2fast);
-    }
-    const double qpp = p0 + dt * r.p, qpn = qpp - pcs, qun = qc[0] + dt * r.u, qvn = qc[1] + dt * r.v, qwn = qc[2] + dt * r.w,
-                 qtn = qc[3] + dt * r.t;
+    double uc, vc, wc, tc;
+    // warp-uniform path choice: plain, x walls only (the x-wall tile columns),
+    // or any wall (y-wall rows, z-wall planes)
+#define CAV_RES(WX, WYZ)                                                                                    \
+  {                                                                                                         \
+    const SmemAcc<QF, WX, WYZ> sa{slot(slk), qslot(slm), qslot(slk), qslot(slp), p0, pzm, pzp, pzm2, pzp2, \
+                                  wfl | zf, a.walls.t_hot, a.walls.t_cold};                                 \
+    r = residual_t(sa, a.sp, s2fast);                                                                       \
+    uc = sa.u();                                                                                            \
+    vc = sa.v();                                                                                            \
+    wc = sa.w();                                                                                            \
+    tc = sa.t();                                                                                            \
+  }
+    if (wyz || zf) CAV_RES(true, true)
+    else if (wx) CAV_RES(true, false)
+    else CAV_RES(false, false)
+#undef CAV_RES
+    const double qpp = p0 + dt * r.p, qpn = qpp - pcs, qun = uc + dt * r.u, qvn = vc + dt * r.v, qwn = wc + dt * r.w,
+                 qtn = tc + dt * r.t;
     // explicit global (streaming) stores: no possible aliasing with the
     // shared-memory ring, so the two cells of a step can interleave
     __stcs(op, qpn);
@@ -485,90 +542,57 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
             (w.wall[2] && j == 2 ? kYlo2 : 0) | (w.wall[2] && j == 3 ? kYlo3 : 0) |
             (w.wall[3] && j == g.ny + 1 ? kYhi1 : 0) | (w.wall[3] && j == g.ny ? kYhi0 : 0);
       if (!active) wfl = 0;
-      wwarp = __any_sync(0xffffffffu, wfl != 0);
+      wx = __any_sync(0xffffffffu, (wfl & (kYlo2 - 1)) != 0);
+      wyz = __any_sync(0xffffffffu, (wfl & ~(kYlo2 - 1)) != 0);
     }
-    // prologue: planes kb-2 .. kb+1
+    // prologue: planes kb-2 .. kb+1; p window from all four, the slots of
+    // kb-1 .. kb+1 stay held for u,v,w,T
     int sa[2], sb[2];
     wait_planes(it, it.kb - 2, 2, sa);
     wait_planes(it, it.kb, 2, sb);
-    const int s0 = sa[0], s1 = sa[1], s2 = sb[0], s3 = sb[1];
-    double P[6];     // p at planes k-2 .. k+3
-    double Q[4][4];  // u,v,w,T at planes k-1 .. k+2
-    P[0] = slot(s0)[0];
-    P[1] = slot(s1)[0];
-    P[2] = slot(s2)[0];
-    P[3] = slot(s3)[0];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      Q[f][0] = qslot(s1)[f * QF];
-      Q[f][1] = qslot(s2)[f * QF];
-    }
-    release_slot(s0);
-    release_slot(s1);
-    int sc0 = s2, sc1 = s3;  // slots of planes k, k+1
+    double P[6];  // p at planes k-2 .. k+3
+    P[0] = slot(sa[0])[0];
+    P[1] = slot(sa[1])[0];
+    P[2] = slot(sb[0])[0];
+    P[3] = slot(sb[1])[0];
+    release_slot(sa[0]);
+    int skm = sa[1], sk0 = sb[0], sk1 = sb[1];  // slots of planes k-1, k, k+1
     double* op = a.out + g.idx(i, j, it.kb);
     int st = 0;
     for (; st + 1 < len; st += 2, op += 2 * plane) {
       const int k = it.kb + st;
       int sn[2];
       wait_planes(it, k + 2, 2, sn);  // planes k+2, k+3
-      const int sc2 = sn[0], sc3 = sn[1];
-      P[4] = slot(sc2)[0];
-      P[5] = slot(sc3)[0];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        Q[f][2] = qslot(sc1)[f * QF];
-        Q[f][3] = qslot(sc2)[f * QF];
-      }
-      if ((zlo && k <= 3) || (zhi && k + 3 >= g.nz + 2)) zwall2(P, Q, k);
+      P[4] = slot(sn[0])[0];
+      P[5] = slot(sn[1])[0];
+      if ((zlo && k <= 3) || (zhi && k + 3 >= g.nz + 2)) zwall2(P, k);
       if (active) {
-        const double qa[4] = {Q[0][1], Q[1][1], Q[2][1], Q[3][1]};
-        const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
-        const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
-        const double qbp[4] = {Q[0][3], Q[1][3], Q[2][3], Q[3][3]};
-        cell(sc0, P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
-        cell(sc1, P[3], P[2], P[4], P[1], P[5], qap, qa, qbp, op + plane, ccol && k + 1 == a.cz);
+        cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
+        cell(sk0, sk1, sn[0], k + 1, P[3], P[2], P[4], P[1], P[5], op + plane, ccol && k + 1 == a.cz);
       }
-      release_slot(sc0);
-      release_slot(sc1);
-      sc0 = sc2;
-      sc1 = sc3;
+      release_slot(skm);
+      release_slot(sk0);
+      skm = sk1;
+      sk0 = sn[0];
+      sk1 = sn[1];
       P[0] = P[2];
       P[1] = P[3];
       P[2] = P[4];
       P[3] = P[5];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        Q[f][0] = Q[f][2];
-        Q[f][1] = Q[f][3];
-      }
     }
     if (st < len) {  // odd remainder: one plane
       const int k = it.kb + st;
       int sn[2];
       wait_planes(it, k + 2, 1, sn);  // plane k+2
-      const int sc2 = sn[0];
-      P[4] = slot(sc2)[0];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) Q[f][2] = qslot(sc1)[f * QF];
-      if ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2)) zwall1(P, Q, k);
-      if (active) {
-        const double qa[4] = {Q[0][1], Q[1][1], Q[2][1], Q[3][1]};
-        const double qam[4] = {Q[0][0], Q[1][0], Q[2][0], Q[3][0]};
-        const double qap[4] = {Q[0][2], Q[1][2], Q[2][2], Q[3][2]};
-        cell(sc0, P[2], P[1], P[3], P[0], P[4], qa, qam, qap, op, ccol && k == a.cz);
-      }
-      release_slot(sc0);
-      sc0 = sc1;
-      sc1 = sc2;
-      // remaining entries: plane k+1 (sc0 now) was waited; plane k+2 (sc1) waited
-      release_slot(sc0);
-      release_slot(sc1);
-    } else {
-      // planes ke, ke+1 (sc0, sc1) served only as column values
-      release_slot(sc0);
-      release_slot(sc1);
+      P[4] = slot(sn[0])[0];
+      if ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2)) zwall1(P, k);
+      if (active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
+      release_slot(sn[0]);
     }
+    // planes ke-1 .. ke+1 (odd: plus ke+2 above) served only as neighbours
+    release_slot(skm);
+    release_slot(sk0);
+    release_slot(sk1);
   }
   constexpr unsigned EXP = 0x7FF00000u;
   unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
