@@ -52,7 +52,7 @@ struct StepArgs {
   double* out;
   Geo g;
   cav_stencil_params sp;
-  double s2fast;  // beta shortcut threshold (host::beta_fast_s2)
+  BetaFast bf;  // beta shortcuts (host::beta_fast)
   cav_box box;
   int kchunk;
   const IterScalars* sc;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
       st.typ = BT[QW];
       st.tzm = tm1;
       st.tzp = tp1;
-      const Res r = residual_of(st, a.sp, a.s2fast);
+      const Res r = residual_of(st, a.sp, a.bf);
       // euler_step: q = q + dt*r (src/solver.cpp:239-246)
       const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
                    qt = t0 + dt * r.t;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
       out[2 * fs + c] = qv;
       out[3 * fs + c] = qw;
       out[4 * fs + c] = qt;
-      const Denoms d = cfl_denoms(qu, qv, qw, u_ref, a.s2fast);
+      const Denoms d = cfl_denoms(qu, qv, qw, u_ref, a.bf);
       m0 = dmax_d(m0, d.du);
       m1 = dmax_d(m1, d.dv);
       m2 = dmax_d(m2, d.dw);
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a
     const double pc = s.sc->pc, dt = s.sc->dt;
     Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
     if (near_wall(a.walls, g, i, j, k)) apply_wall_ghosts(st, a.walls, g, i, j, k);
-    const Res r = residual_of(st, s.sp, s.s2fast);
+    const Res r = residual_of(st, s.sp, s.bf);
     const double qp = st.p + dt * r.p, qu = st.u + dt * r.u, qv = st.v + dt * r.v, qw = st.w + dt * r.w,
                  qt = st.t + dt * r.t;
     const long long c = g.idx(i, j, k);
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a
     s.out[2 * fs + c] = qv;
     s.out[3 * fs + c] = qw;
     s.out[4 * fs + c] = qt;
-    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref, s.s2fast);
+    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref, s.bf);
     m0 = d.du;
     m1 = d.dv;
     m2 = d.dw;
@@ -679,9 +679,9 @@ cudaEvent_t make_event() {
 
 // pcs_1 = p'(centre) of the first step (eager mode; later ones are folded by
 // the step kernel's last CTA).
-__global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, double s2fast,
+__global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, BetaFast bf,
                              IterScalars* sc, int cx, int cy, int cz) {
-  if (threadIdx.x == 0) sc->pcs = center_p_update(state, g, w, sp, s2fast, sc->dt, 0.0, cx, cy, cz);
+  if (threadIdx.x == 0) sc->pcs = center_p_update(state, g, w, sp, bf, sc->dt, 0.0, cx, cy, cz);
 }
 
 int getenv_int(const char* name, int dflt) {
@@ -796,7 +796,7 @@ struct Block {
   int kind_ty = 8;
   int kchunk = 0;
   CUtensorMap tmap[2][2];  // [state][p, uvwT]
-  double s2fast = -1.0;
+  BetaFast bf{-1.0, 0u};
   bool eager = false;            // single-rank TMA pipeline: rescaled p stored directly
   WallInfo winfo{};
   int tma_grid = 0;
@@ -843,7 +843,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     cz = c[2] - e.lo[2] + 2;
   }
   sp = host::stencil_params(dx, dy, dz, d.fluid);
-  s2fast = host::beta_fast_s2(sp.u_ref);
+  bf = host::beta_fast(sp.u_ref);
   plan = host::build_plan(n, rank_at, d.strategy);
   host::overlap_regions(n, rank_at, &internal, shells);
   lay = arena_layout(plan, d.np);
@@ -1051,7 +1051,7 @@ void Block::prologue() {
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
   if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
-    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, s2fast, sc + 1, cx, cy, cz);
+    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, sc + 1, cx, cy, cz);
     CAV_CUDA(cudaGetLastError());
   }
   primed = true;
@@ -1066,7 +1066,7 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.out = state[cur ^ 1];
     a.g = g;
     a.sp = sp;
-    a.s2fast = s2fast;
+    a.bf = bf;
     a.work = counters + 62;
     a.eager = eager ? 1 : 0;
     a.box = box;
@@ -1124,7 +1124,7 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
   a.out = state[cur ^ 1];
   a.g = g;
   a.sp = sp;
-  a.s2fast = s2fast;
+  a.bf = bf;
   a.box = box;
   a.sc = sc + (it & 1);
   a.acc = acc + (it & 1);
@@ -1150,7 +1150,7 @@ void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
   a.s.out = state[cur ^ 1];
   a.s.g = g;
   a.s.sp = sp;
-  a.s.s2fast = s2fast;
+  a.s.bf = bf;
   a.s.sc = sc + (it & 1);
   a.s.acc = acc + (it & 1);
   a.s.digits = dig;
@@ -1279,7 +1279,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
   if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
-    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, s2fast, sc + 1, cx, cy, cz);
+    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, sc + 1, cx, cy, cz);
     CAV_CUDA(cudaGetLastError());
   }
   cur ^= 1;

@@ -38,11 +38,20 @@ struct Res {
 // expressions are evaluated is grouped per equation, which keeps fewer values
 // live and cannot change any result.
 //
-// beta = max(sqrt(s2), u_ref) (compute_beta, include/cavity/solver.hpp:73-75).
-// `s2fast` is the largest double whose correctly rounded square root is still
-// below u_ref (host: beta_fast_s2); for s2 <= s2fast, beta is u_ref exactly
-// (sqrt is monotone), so the IEEE sqrt sequence is skipped. A negative s2fast
-// disables the shortcut; NaN s2 always takes the full path.
+// beta = max(sqrt(s2), u_ref) (compute_beta, include/cavity/solver.hpp:73-75)
+// with two exact shortcuts (BetaFast, host: host::beta_fast):
+//  * hb: when |u|, |v|, |w| all have a high word below hi(u_ref/2), each is
+//    below u_ref/2, so s2 <= 3/4 u_ref^2 (+ rounding) < s2 and beta is u_ref:
+//    decided with integer ops on the high words, s2 itself is never formed;
+//  * s2: the largest double whose correctly rounded square root is still
+//    below u_ref; for s2' <= s2 beta is u_ref (sqrt is monotone), so the IEEE
+//    sqrt sequence is skipped. NaN always takes the full path.
+// {-1, 0} disables both.
+struct BetaFast {
+  double s2;
+  unsigned hb;
+};
+
 // The square root is volatile inline PTX (sqrt.rn.f64, the same correctly
 // rounded operation) so the compiler cannot hoist it above the branch and
 // if-convert: at quiescent cells s2 == 0, which would otherwise run the IEEE
@@ -52,16 +61,26 @@ __device__ __forceinline__ double sqrt_rn(double x) {
   asm volatile("sqrt.rn.f64 %0, %1;" : "=d"(r) : "d"(x));
   return r;
 }
-__device__ __forceinline__ double beta_of(double s2, double u_ref, double s2fast) {
+// true unless |u|, |v|, |w| < u_ref/2 is certain from the high words
+__device__ __forceinline__ bool speed_not_small(double u, double v, double w, unsigned hb) {
+  const unsigned a = static_cast<unsigned>(__double2hiint(u)) & 0x7FFFFFFFu;
+  const unsigned b = static_cast<unsigned>(__double2hiint(v)) & 0x7FFFFFFFu;
+  const unsigned c = static_cast<unsigned>(__double2hiint(w)) & 0x7FFFFFFFu;
+  return max(max(a, b), c) >= hb;
+}
+__device__ __forceinline__ double beta_of(double u, double v, double w, double u_ref, const BetaFast& bf) {
   double b = u_ref;
-  if (!(s2 <= s2fast)) b = smax(sqrt_rn(s2), u_ref);
+  if (speed_not_small(u, v, w, bf.hb)) {
+    const double s2 = (u * u + v * v) + w * w;
+    if (!(s2 <= bf.s2)) b = smax(sqrt_rn(s2), u_ref);
+  }
   return b;
 }
 
 template <class S>
-__device__ __forceinline__ Res residual_t(const S& s, const cav_stencil_params& q, double s2fast = -1.0) {
+__device__ __forceinline__ Res residual_t(const S& s, const cav_stencil_params& q, const BetaFast& bf = {-1.0, 0u}) {
   const double uc = s.u(), vc = s.v(), wc = s.w(), tc = s.t();
-  const double b = beta_of((uc * uc + vc * vc) + wc * wc, q.u_ref, s2fast);
+  const double b = beta_of(uc, vc, wc, q.u_ref, bf);
   const double b2 = b * b;
   Res r;
   // continuity + fourth-difference damping
@@ -141,8 +160,9 @@ struct StarAcc {
 #undef CAV_A
 };
 
-__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q, double s2fast = -1.0) {
-  return residual_t(StarAcc{s}, q, s2fast);
+__device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_params& q,
+                                          const BetaFast& bf = {-1.0, 0u}) {
+  return residual_t(StarAcc{s}, q, bf);
 }
 
 // compute_beta (include/cavity/solver.hpp:73-75) and the per-cell CFL
@@ -153,8 +173,9 @@ __device__ __forceinline__ Res residual_of(const Star& s, const cav_stencil_para
 struct Denoms {
   double du, dv, dw;
 };
-__device__ __forceinline__ Denoms cfl_denoms(double u, double v, double w, double u_ref, double s2fast = -1.0) {
-  const double b = beta_of((u * u + v * v) + w * w, u_ref, s2fast);
+__device__ __forceinline__ Denoms cfl_denoms(double u, double v, double w, double u_ref,
+                                             const BetaFast& bf = {-1.0, 0u}) {
+  const double b = beta_of(u, v, w, u_ref, bf);
   return {fabs(u) + b, fabs(v) + b, fabs(w) + b};
 }
 

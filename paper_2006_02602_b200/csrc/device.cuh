@@ -185,12 +185,12 @@ __device__ __forceinline__ bool near_wall(const WallInfo& w, const Geo& g, int i
 // the fly. Used to obtain the centre pressure pc_n before the step that
 // stores fl(p' - pc_n) (rescale_pressure, src/solver.cpp:248-257).
 __device__ __forceinline__ double center_p_update(const double* state, const Geo& g, const WallInfo& w,
-                                                  const cav_stencil_params& sp, double s2fast, double dt,
+                                                  const cav_stencil_params& sp, const BetaFast& bf, double dt,
                                                   double pc_lazy, int i, int j, int k) {
   const long long fs = g.fstride;
   Star st = load_star(state, state + fs, state + 2 * fs, state + 3 * fs, state + 4 * fs, g, i, j, k, pc_lazy);
   if (near_wall(w, g, i, j, k)) apply_wall_ghosts(st, w, g, i, j, k);
-  const Res r = residual_of(st, sp, s2fast);
+  const Res r = residual_of(st, sp, bf);
   return st.p + dt * r.p;
 }
 

@@ -141,6 +141,17 @@ double beta_fast_s2(double u_ref) {
   return s;
 }
 
+BetaFast beta_fast(double u_ref) {
+  BetaFast bf{beta_fast_s2(u_ref), 0u};
+  if (u_ref >= 1e-100 && u_ref <= 1e100) {  // u_ref/2 and its squares stay normal
+    const double h = u_ref * 0.5;
+    uint64_t bits;
+    std::memcpy(&bits, &h, sizeof bits);
+    bf.hb = static_cast<unsigned>(bits >> 32);
+  }
+  return bf;
+}
+
 std::array<int, 3> choose_dims(int np, int mode) {
   if (np < 1) throw std::invalid_argument("choose_dims: np must be >= 1");
   switch (mode) {

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "cavity_b200.h"
+#include "cell.cuh"
 
 namespace cav::host {
 
@@ -32,6 +33,8 @@ cav_stencil_params stencil_params(double dx, double dy, double dz, const cav_flu
 // max(sqrt(s'), u_ref) == u_ref for every s' <= s; -1 when u_ref is not a
 // positive finite number (the device then always takes the full sqrt).
 double beta_fast_s2(double u_ref);
+// BetaFast shortcuts for u_ref: {beta_fast_s2, high word of u_ref/2} (cell.cuh).
+BetaFast beta_fast(double u_ref);
 
 // choose_dims (src/decomp.cpp:67-98).
 std::array<int, 3> choose_dims(int np, int mode);

@@ -132,7 +132,7 @@ struct TmaStepArgs {
   double* out;
   Geo g;
   cav_stencil_params sp;
-  double s2fast;  // beta shortcut threshold (host::beta_fast_s2)
+  BetaFast bf;  // beta shortcuts (host::beta_fast)
   unsigned* work;  // dynamic item counter (items >= gridDim.x), reset by the last CTA
   int eager;      // store fl(p' - sc->pcs) and fold pcs_{n+1} (single rank); see IterScalars
   cav_box box;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // residuals interleave.
   const int tx = lane, ty = warp;
   const Geo g = a.g;
-  const double dt = a.sc->dt, u_ref = a.sp.u_ref, s2fast = a.s2fast, pcs = a.sc->pcs;
+  const double dt = a.sc->dt, u_ref = a.sp.u_ref, pcs = a.sc->pcs;
   const long long fs = g.fstride;
   const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
   const bool zlo = a.walls.wall[4], zhi = a.walls.wall[5];
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   {                                                                                                         \
     const SmemAcc<QF, WX, WYZ> sa{slot(slk), qslot(slm), qslot(slk), qslot(slp), p0, pzm, pzp, pzm2, pzp2, \
                                   wfl | zf, a.walls.t_hot, a.walls.t_cold};                                 \
-    r = residual_t(sa, a.sp, s2fast);                                                                       \
+    r = residual_t(sa, a.sp, a.bf);                                                                       \
     uc = sa.u();                                                                                            \
     vc = sa.v();                                                                                            \
     wc = sa.w();                                                                                            \
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     __stcs(op + 2 * fs, qvn);
     __stcs(op + 3 * fs, qwn);
     __stcs(op + 4 * fs, qtn);
-    const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, s2fast);
+    const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, a.bf);
     m0 = dmax_d(m0, d.du);
     m1 = dmax_d(m1, d.dv);
     m2 = dmax_d(m2, d.dw);
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
           // this iteration's output is final; pcs_{n+1} = p'(centre) of the
           // next step, from the same inputs and arithmetic as that step
           a.sc_next->pc = 0.0;
-          a.sc_next->pcs = a.rescale ? center_p_update(a.out, a.g, a.walls, a.sp, a.s2fast, dtn, 0.0, a.cx,
+          a.sc_next->pcs = a.rescale ? center_p_update(a.out, a.g, a.walls, a.sp, a.bf, dtn, 0.0, a.cx,
                                                        a.cy, a.cz)
                                      : 0.0;
         } else {
