@@ -63,6 +63,10 @@ _LL = C.c_longlong
 
 
 def lib_path(fmad=False):
+    # CAV_LIB: an alternate build of the same library (A/B timing of two builds in one run)
+    alt = os.environ.get("CAV_LIB")
+    if alt and not fmad:
+        return alt
     return os.path.join(LIB_DIR, LIB_FMAD_NAME if fmad else LIB_NAME)
 
 
