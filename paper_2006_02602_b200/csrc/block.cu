@@ -798,6 +798,7 @@ struct Block {
   CUtensorMap tmap[2][2];  // [state][p, uvwT]
   BetaFast bf{-1.0, 0u};
   bool eager = false;            // single-rank TMA pipeline: rescaled p stored directly
+  int tail_chunks = -1;          // CAV_TAIL_CHUNKS: short chunks at the end (-1 = two waves)
   WallInfo winfo{};
   int tma_grid = 0;
   int tma_variant = 0;
@@ -889,6 +890,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");
     use_tma = !(k && std::string(k) == "tiled");
+    tail_chunks = getenv_int("CAV_TAIL_CHUNKS", -1);
     const char* ea = std::getenv("CAV_EAGER");
     eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
     const char* os = std::getenv("CAV_OVERLAP_STREAMS");
@@ -1095,7 +1097,19 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
         a.chunk = L;
       }
     }
-    a.nchunks = (bd + a.chunk - 1) / a.chunk;
+    // tail: about two waves' worth of short items at the end of the order
+    {
+      const int ls = std::max(4, a.chunk / 4);
+      int nsmall = tail_chunks >= 0 ? tail_chunks
+                                    : static_cast<int>((2LL * tma_grid + a.ntiles - 1) / a.ntiles);
+      nsmall = std::min(nsmall, (bd / 2) / ls);  // keep most of the box in long items
+      if (a.chunk <= ls) nsmall = 0;
+      const int bigext = bd - nsmall * ls;
+      a.nbig = (bigext + a.chunk - 1) / a.chunk;
+      a.bigend = box.lo[2] + bigext;
+      a.chunk_tail = ls;
+      a.nchunks = a.nbig + nsmall;
+    }
     a.walls = winfo;
     a.fold = d.np == 1 ? 1 : 0;
     a.done = counters + 63;

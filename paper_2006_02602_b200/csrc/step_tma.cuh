@@ -118,9 +118,11 @@ template <int TY_, int R_, int CTAS_>
 struct TmaCfg {
   static constexpr int TY = TY_, R = R_, CTAS = CTAS_;
   static constexpr int PH = TY + 4, QH = TY + 2;
-  static constexpr int PField = kPW * PH;     // doubles of the p part
+  static constexpr int PHA = (PH + 3) / 4 * 4;  // p rows allotted: keeps the u..T box 128-byte aligned
+  static constexpr int PField = kPW * PHA;      // doubles of the p part
   static constexpr int QField = kQW * QH;     // doubles per u/v/w/T part
   static constexpr int Slot = PField + 4 * QField;
+  static constexpr int TxBytes = (kPW * PH + 4 * QField) * 8;  // bytes the two boxes deliver
   static constexpr int Threads = 32 * (TY + 1);  // consumers + issuer
   static constexpr int NC = 32 * TY;              // consumer threads
   static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + 5 * kDigits * 8;
@@ -143,6 +145,11 @@ struct TmaStepArgs {
   long long n;
   int rank;
   int tiles_x, ntiles, chunk, nchunks;
+  // chunks [0, nbig) have `chunk` planes from box.lo[2] (the last one may be
+  // shorter, ending at bigend); chunks >= nbig have `chunk_tail` planes from
+  // bigend: the items claimed last are short, which shortens the tail where
+  // CTAs run out of work at different times
+  int nbig, chunk_tail, bigend;
   WallInfo walls;
   // single-rank fold (replaces k_scalar_sync when np == 1): the last CTA to
   // finish turns this iteration's maxima into dt_{n+1} and publishes pc_n
@@ -166,8 +173,13 @@ __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long it
   ItemGeom r;
   r.ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
   r.tj0 = a.box.lo[1] + (tile / a.tiles_x) * TY;
-  r.kb = a.box.lo[2] + chunk * a.chunk;
-  r.ke = min(r.kb + a.chunk, a.box.hi[2]);
+  if (chunk < a.nbig) {
+    r.kb = a.box.lo[2] + chunk * a.chunk;
+    r.ke = min(r.kb + a.chunk, a.bigend);
+  } else {
+    r.kb = a.bigend + (chunk - a.nbig) * a.chunk_tail;
+    r.ke = min(r.kb + a.chunk_tail, a.box.hi[2]);
+  }
   return r;
 }
 
@@ -316,7 +328,7 @@ __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, cons
     q.fin = true;
   } else {
     sitem[q.s] = q.item;
-    tma::mbar_expect_tx(&full[q.s], Cfg::Slot * sizeof(double));
+    tma::mbar_expect_tx(&full[q.s], Cfg::TxBytes);
     double* dst = ring + q.s * Cfg::Slot;
     const int x0 = a.g.off + q.it.ti0 - 2, y0 = q.it.tj0 - 2;
     tma::load_4d(dst, mP, x0, y0, q.pl, 0, &full[q.s]);
