@@ -623,6 +623,20 @@ __global__ void k_export(const double* cur, const double* prev, Geo g, double pc
   out[q] = x;
 }
 
+// Host Field3 layout (contiguous, i-fastest, 5 fields) -> both padded states.
+__global__ void k_import(const double* in, double* s0, double* s1, Geo g) {
+  const long long X = g.nx + 4, Y = g.ny + 4, Z = g.nz + 4, S = X * Y * Z;
+  const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (q >= 5 * S) return;
+  const int v = static_cast<int>(q / S);
+  const long long e = q % S;
+  const int i = static_cast<int>(e % X), j = static_cast<int>((e / X) % Y), k = static_cast<int>(e / (X * Y));
+  const long long c = v * g.fstride + g.idx(i, j, k);
+  const double x = in[q];
+  s0[c] = x;
+  s1[c] = x;
+}
+
 __global__ void k_fill_ic(double* s0, double* s1, Geo g, double t_inf) {
   const long long X = g.nx + 4, Y = g.ny + 4, Z = g.nz + 4, S = X * Y * Z;
   const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -885,6 +899,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_scalar_sync));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_import));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_center_pcs));
   }
   {
@@ -1408,11 +1423,15 @@ int cav_block_upload(cav_block* bh, const double* host5) {
   return guarded([&] {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
-    const size_t X = b.n[0] + 4, Y = b.n[1] + 4, Z = b.n[2] + 4;
-    for (int s = 0; s < 2; ++s)
-      for (int v = 0; v < 5; ++v)
-        CAV_CUDA(cudaMemcpy2DAsync(b.field(s, v) + b.g.off, b.g.pitch * sizeof(double), host5 + v * X * Y * Z,
-                                   X * sizeof(double), X * sizeof(double), Y * Z, cudaMemcpyHostToDevice, b.s0));
+    // one contiguous host->device copy (full PCIe rate, no 2-D row DMA), then
+    // a device scatter into both padded states
+    const long long S = static_cast<long long>(b.n[0] + 4) * (b.n[1] + 4) * (b.n[2] + 4);
+    double* tmp = nullptr;
+    CAV_CUDA(cudaMallocAsync(&tmp, 5 * S * sizeof(double), b.s0));
+    CAV_CUDA(cudaMemcpyAsync(tmp, host5, 5 * S * sizeof(double), cudaMemcpyHostToDevice, b.s0));
+    k_import<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(tmp, b.state[0], b.state[1], b.g);
+    CAV_CUDA(cudaGetLastError());
+    CAV_CUDA(cudaFreeAsync(tmp, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));  // ordered with this block's non-blocking streams
     b.cur = 0;
     b.next_n = 1;
