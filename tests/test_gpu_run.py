@@ -207,3 +207,37 @@ def test_fmad_tolerance_build_within_1e10(golden, golden_arrays, name):
     want = np.array([[float.fromhex(x) for x in row] for row in entry["history"]])
     rel = np.abs(r.history - want) / np.maximum(np.abs(want), 1e-300)
     assert np.all(rel[want != 0] <= 1e-10)
+
+
+# ---- BASELINE.json configs[1] at its full size (256^3) -----------------------
+
+C1 = (256, 256, 256)
+
+
+def test_c1_full_size_matches_oracle_bitwise():
+    """configs[1]'s grid, a few iterations with the residual-norm history at
+    every step: fields and norms bitwise equal to the C oracle (which is itself
+    pinned to the reference, tests/test_oracle.py). Exercises the production
+    TMA step at its benchmark size: all tile classes, dynamic items, tail
+    chunks, eager rescale and the last-CTA fold."""
+    cfg = capi.default_config(grid=C1, steps=5, check_every=1)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True)
+    o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
+    assert list(r.history_iter) == list(o["history_iter"])
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+
+
+@pytest.mark.parametrize("np_, mode, overlap", [(2, "1d-i", 1), (8, "3d", 1), (4, "2d", 0)])
+def test_c1_full_size_decomposition_independent(np_, mode, overlap):
+    """Size-independent property at full size: the reference is bitwise
+    independent of decomposition (P/README.md:10-15), so every rank layout of
+    the 256^3 case reproduces the single-rank fields and norms bit for bit
+    (ranks share device 0 here; the halo exchange, lazy rescale and scalar
+    sync are the multi-GPU code path)."""
+    base = capi.default_config(grid=C1, steps=4, check_every=2)
+    one = capi.run_case(base, collect_fields=True, collect_history=True)
+    many = capi.run_case(capi.default_config(grid=C1, steps=4, check_every=2, np=np_, mode=mode, strategy="v3",
+                                             overlap=overlap), collect_fields=True, collect_history=True)
+    np.testing.assert_array_equal(bits(many.fields), bits(one.fields))
+    np.testing.assert_array_equal(bits(many.history), bits(one.history))
