@@ -7,8 +7,7 @@
 // slots with two cp.async.bulk.tensor.4d boxes — p as 36 x (TY+4) (2-cell
 // halo ring) and u,v,w,T as 4 x 36 x (TY+2) (1-cell y ring), i.e. only the
 // halo each variable's stencil reads (completion = the slot's `full` mbarrier
-// transaction count); it only waits for a slot to be released (`empty`). An
-// optional second cursor prefetches planes ahead into L2.
+// transaction count); it only waits for a slot to be released (`empty`).
 //
 // Consumer warps wait on `full` directly and never write the ring: the x/y
 // wall ghosts of apply_boundary_conditions (src/solver.cpp:158-191) are formed
@@ -21,16 +20,17 @@
 //
 // Each consumer keeps its column's p k-window in registers (k-2..k+3; z-wall
 // ghosts are formed there) and reads u,v,w,T at k-1..k+1 from the slots it
-// holds (planes k-1..k+3, five slots), computes two planes per step,
-// residual_t (cell.cuh, the
-// reference's arithmetic), the Euler update, the next step's CFL maxima and
-// the non-finite flags, stores, and releases the slots (`empty` mbarrier).
+// holds (planes k-1..k+3, five slots), and computes two planes per step:
+// residual_t (cell.cuh, the reference's arithmetic), the Euler update, the
+// next step's CFL maxima and the non-finite flags; it stores and releases the
+// slots (`empty` mbarrier).
 //
 // Work: items are (k-chunk, tile) in chunk-major order; CTA c starts with item
 // c, then takes the next unclaimed item from a global counter, so the ~G items
 // in flight at any time are neighbouring tiles of the same chunk (their halo
 // rows are L2 hits), slower items (wall tiles) do not unbalance the SMs, and
-// each item restarts the k-window once.
+// each item restarts the k-window once. The last items in the order are
+// short k-chunks, which shortens the tail where CTAs run out of work.
 #pragma once
 
 #include <cuda.h>
@@ -70,19 +70,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(1000000u)
       : "memory");
 }
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t r;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(r)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return r != 0;
-}
 __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int x, int y, int z, int f,
                                         uint64_t* bar) {
   asm volatile(
@@ -90,13 +77,6 @@ __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int x
       "[%6];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(f), "r"(smem_u32(bar))
       : "memory");
-}
-// L2-only prefetch of one box (no shared-memory destination, no completion).
-__device__ __forceinline__ void prefetch_4d(const CUtensorMap* map, int x, int y, int z, int f) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(x), "r"(y), "r"(z), "r"(f)
-               : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
@@ -296,7 +276,7 @@ __device__ __forceinline__ bool plane_needs_rescale(const TmaStepArgs& a, int pl
 
 // TMA issue cursor of the issuer warp (lane 0). (Measured: folding it into
 // consumer warp 0 to free a warp slot was 16% slower — the ring is only fed
-// when that warp reaches a wait.) Items:
+// when that warp reaches a wait; DESIGN.md §3.) Items:
 // blockIdx.x first, then dynamically from a.work (wall tiles and the odd
 // item out make a static round-robin uneven). Each entry's item id goes to
 // sitem[] before the slot's arrive, which releases it to the consumers'
@@ -310,18 +290,14 @@ struct Issuer {
   bool done, fin;
 };
 
-// Issues the next entry if its slot is free (or after waiting for it when
-// `block`); false when nothing was issued.
+// Issues the next entry once its slot is free; false after the sentinel.
 template <class Cfg>
 __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, const CUtensorMap* mQ,
                                           const TmaStepArgs& a, double* ring, uint64_t* full, uint64_t* empty,
-                                          long long* sitem, long long total, bool block) {
+                                          long long* sitem, long long total) {
   constexpr int R = Cfg::R;
   if (q.fin) return false;
-  if (q.e >= static_cast<uint32_t>(R)) {
-    if (block) tma::mbar_wait(&empty[q.s], q.ph ^ 1);
-    else if (!tma::mbar_test(&empty[q.s], q.ph ^ 1)) return false;
-  }
+  if (q.e >= static_cast<uint32_t>(R)) tma::mbar_wait(&empty[q.s], q.ph ^ 1);
   if (q.done) {
     sitem[q.s] = -1;
     tma::mbar_arrive(&full[q.s]);
@@ -391,7 +367,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       iq.it = item_geom<C>(a, iq.item);
       iq.pl = iq.it.kb - 2;
     }
-    while (issue_one<Cfg>(iq, &mapP, &mapQ, a, ring, full, empty, sitem, total, true)) {
+    while (issue_one<Cfg>(iq, &mapP, &mapQ, a, ring, full, empty, sitem, total)) {
     }
     return;
   }
