@@ -549,15 +549,19 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     int st = 0;
     for (; st + 1 < len; st += 2, op += 2 * plane) {
       const int k = it.kb + st;
+      // plane k+3 is awaited only after cell k is done: cell k needs planes
+      // k-1..k+2, cell k+1 also k+3, so the later plane gets a cell's worth
+      // of extra time to land. The z-wall rules read P[0..4] only; a ghost
+      // P[5] they form (k+3 >= nz+2) is not overwritten by the slot.
       int sn[2];
-      wait_planes(it, k + 2, 2, sn);  // planes k+2, k+3
+      wait_planes(it, k + 2, 1, sn);
       P[4] = slot(sn[0])[0];
-      P[5] = slot(sn[1])[0];
-      if ((zlo && k <= 3) || (zhi && k + 3 >= g.nz + 2)) zwall2(P, k);
-      if (active) {
-        cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
-        cell(sk0, sk1, sn[0], k + 1, P[3], P[2], P[4], P[1], P[5], op + plane, ccol && k + 1 == a.cz);
-      }
+      const bool zh5 = zhi && k + 3 >= g.nz + 2;
+      if ((zlo && k <= 3) || zh5) zwall2(P, k);
+      if (active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
+      wait_planes(it, k + 3, 1, sn + 1);
+      if (!zh5) P[5] = slot(sn[1])[0];
+      if (active) cell(sk0, sk1, sn[0], k + 1, P[3], P[2], P[4], P[1], P[5], op + plane, ccol && k + 1 == a.cz);
       release_slot(skm);
       release_slot(sk0);
       skm = sk1;
