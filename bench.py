@@ -309,10 +309,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         capi.check(b2.L.cav_block_upload(b2.h, C.cast(host_in.data_ptr(), C.POINTER(C.c_double))))
+        t1 = time.perf_counter()
         b2.next_it = 1
         b2.run(args.steps)
+        t2 = time.perf_counter()
         capi.check(b2.L.cav_block_download(b2.h, C.cast(host_out.data_ptr(), C.POINTER(C.c_double))))
-        wall = time.perf_counter() - t0
+        t3 = time.perf_counter()
+        wall = t3 - t0
+        parts = {"upload_s": t1 - t0, "run_s": t2 - t1, "download_s": t3 - t2}  # each call is synchronous
         w = torch.tensor([wall], dtype=torch.float64)
         if dist:
             dist.all_reduce(w, op=dist.ReduceOp.MAX)
@@ -322,7 +326,7 @@ def run_ours(args):
         e2e = {"value": cells * args.steps / wall / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
                "api": "cav_block_upload (pinned host) + cav_block_run + cav_block_download",
-               "wall_s": wall}
+               "wall_s": wall, **parts}
 
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:

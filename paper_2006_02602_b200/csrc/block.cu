@@ -781,6 +781,7 @@ struct Block {
   cav_stencil_params sp{};
   Geo g{};
   double* state[2]{};
+  double* staging = nullptr;  // 5 * S doubles in the host Field3 layout (upload / download)
   int cur = 0;
   std::vector<cav_plan_entry> plan;
   ArenaLayout lay;
@@ -886,6 +887,9 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
     CAV_CUDA(cudaMemsetAsync(state[s], 0, 5 * g.fstride * sizeof(double), s0));
   }
+  // staging for upload/download, allocated once (a per-call allocation of
+  // this size sat inside the e2e timed region)
+  CAV_CUDA(cudaMalloc(&staging, 5 * static_cast<size_t>(n[0] + 4) * (n[1] + 4) * (n[2] + 4) * sizeof(double)));
   {  // load every kernel module now (see ops::preload_kernels)
     ops::preload_kernels();
     cudaFuncAttributes fa;
@@ -961,6 +965,7 @@ Block::~Block() {
   for (auto e : kev) cudaEventDestroy(e);
   cudaFree(state[0]);
   cudaFree(state[1]);
+  cudaFree(staging);
   cudaFree(arena);
   cudaFree(acc);
   cudaFree(sc);
@@ -1426,12 +1431,9 @@ int cav_block_upload(cav_block* bh, const double* host5) {
     // one contiguous host->device copy (full PCIe rate, no 2-D row DMA), then
     // a device scatter into both padded states
     const long long S = static_cast<long long>(b.n[0] + 4) * (b.n[1] + 4) * (b.n[2] + 4);
-    double* tmp = nullptr;
-    CAV_CUDA(cudaMallocAsync(&tmp, 5 * S * sizeof(double), b.s0));
-    CAV_CUDA(cudaMemcpyAsync(tmp, host5, 5 * S * sizeof(double), cudaMemcpyHostToDevice, b.s0));
-    k_import<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(tmp, b.state[0], b.state[1], b.g);
+    CAV_CUDA(cudaMemcpyAsync(b.staging, host5, 5 * S * sizeof(double), cudaMemcpyHostToDevice, b.s0));
+    k_import<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.staging, b.state[0], b.state[1], b.g);
     CAV_CUDA(cudaGetLastError());
-    CAV_CUDA(cudaFreeAsync(tmp, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));  // ordered with this block's non-blocking streams
     b.cur = 0;
     b.next_n = 1;
@@ -1473,13 +1475,10 @@ int cav_block_download(cav_block* bh, double* host5) {
                        b.field(b.cur ^ 1, 4)};
       ops::launch_bc(fp, b.g, b.walls, b.d.fluid, b.sc + ((b.next_n - 1) & 1), b.s0);
     }
-    double* tmp = nullptr;
-    CAV_CUDA(cudaMallocAsync(&tmp, 5 * S * sizeof(double), b.s0));
     k_export<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.state[b.cur], b.state[b.cur ^ 1],
-                                                                           b.g, pc, tmp);
+                                                                           b.g, pc, b.staging);
     CAV_CUDA(cudaGetLastError());
-    CAV_CUDA(cudaMemcpyAsync(host5, tmp, 5 * S * sizeof(double), cudaMemcpyDeviceToHost, b.s0));
-    CAV_CUDA(cudaFreeAsync(tmp, b.s0));
+    CAV_CUDA(cudaMemcpyAsync(host5, b.staging, 5 * S * sizeof(double), cudaMemcpyDeviceToHost, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
   });
 }
