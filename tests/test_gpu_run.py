@@ -241,3 +241,22 @@ def test_c1_full_size_decomposition_independent(np_, mode, overlap):
                                              overlap=overlap), collect_fields=True, collect_history=True)
     np.testing.assert_array_equal(bits(many.fields), bits(one.fields))
     np.testing.assert_array_equal(bits(many.history), bits(one.history))
+
+
+@pytest.mark.parametrize("u_ref, np_", [(1e-3, 1), (0.02, 1), (1e-3, 2)])
+def test_beta_branches_match_oracle(u_ref, np_):
+    """beta = max(|V|, u_ref) (compute_beta): with u_ref below the flow speed
+    (max|V| ~ 0.036 here) the step kernel's exact shortcuts are bypassed —
+    the high-word test fails and s2 exceeds beta_fast_s2 — so the IEEE sqrt
+    branch, the mixed warps and the CFL maxima over sqrt-derived betas are
+    all exercised; u_ref = 0.02 mixes cells on both sides of u_ref/2 and u_ref.
+    Bitwise vs the oracle, fields and norm history."""
+    kw = dict(grid=(24, 20, 16), steps=80, check_every=5, u_ref=u_ref)
+    if np_ > 1:
+        kw.update(np=np_, mode="1d-i", strategy="v3", overlap=1)
+    r = capi.run_case(capi.default_config(**kw), collect_fields=True, collect_history=True)
+    o = Oracle.run_case(capi.default_config(grid=(24, 20, 16), steps=80, check_every=5, u_ref=u_ref),
+                        collect_fields=True, collect_history=True)
+    assert np.abs(o["fields"].reshape(5, -1)[1:4]).max() > u_ref  # the flow does outrun u_ref
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
