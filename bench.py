@@ -343,7 +343,11 @@ def run_ours(args):
                                       capi.version(args.fmad)),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches,
-                "hbm_frac_of_step": BYTES_PER_CELL * cells / (total_ms * 1e-3 / args.steps) / 1e9 / n / peak}
+                "hbm_frac_of_step": BYTES_PER_CELL * cells / (total_ms * 1e-3 / args.steps) / 1e9 / n / peak,
+                # share of the iteration outside the fused step kernel (halo pack/unpack, flag
+                # waits, overlap shells, scalar sync, launch gaps): the exposed-communication
+                # fraction at N > 1 (at N = 1 only launch gaps remain)
+                "exposed_comm_frac": (1.0 - roof["step_share"]) if roof["step_share"] is not None else None}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
