@@ -353,7 +353,6 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   __syncthreads();
 
   const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
-  const long long G = gridDim.x;
   const double pc = a.sc->pc;
   const bool lazy = __double_as_longlong(pc) != 0;
 
@@ -372,10 +371,9 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     return;
   }
   // ---------------- consumers ----------------
-  // Each step computes two planes (k, k+1) of the thread's column: the
-  // k-windows are shared (p: k-2..k+3, u,v,w,T: k-1..k+2), waits/releases and
-  // loop control are paid once per two cells, and the two independent
-  // residuals interleave.
+  // Each step computes two planes (k, k+1) of the thread's column: the p
+  // k-window (k-2..k+3) is shared, and the slot bookkeeping and loop control
+  // are paid once per two cells.
   const int tx = lane, ty = warp;
   const Geo g = a.g;
   const double dt = a.sc->dt, u_ref = a.sp.u_ref, pcs = a.sc->pcs;
@@ -395,17 +393,13 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       ph ^= 1;
     }
   };
-  // Wait for the planes of one step (1 or 2 consecutive entries) to land, then
-  // finalise the ones that need it: all consumer threads patch, a named
-  // barrier per phase makes the patches visible to every consumer warp, and
-  // the writers' proxy fence orders them before the slot's next TMA fill.
+  // Wait for the next 1 or 2 entries to land. With a pending lazy shift
+  // (multi-rank blocks) all consumer threads rescale the landed p tile in
+  // place, a named barrier makes that visible to every consumer warp, and the
+  // writers' proxy fence orders it before the slot's next TMA fill.
   const int tid = threadIdx.x;
   int wfl = 0;         // wall flags of this thread's column (kXlo2 ... kYhi0)
   bool wx = false, wyz = false;  // some lane of this warp has an x / y wall flag (warp-uniform)
-  // Warp 0 keeps the ring fed: everything whose slot is free now, and at
-  // least through entry `need` (blocking on its slot if necessary; the
-  // entries that slot's holders wait for are all issued, so this cannot
-  // deadlock).
   auto wait_planes = [&](const ItemGeom& it, int pl, int count, int* sl) {
     bool any = false;
     for (int q = 0; q < count; ++q) {
