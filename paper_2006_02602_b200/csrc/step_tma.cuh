@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         if (nonfinite(rr[v])) nbad = 1;
-        else add_term_digits(sdig + v * kDigits, rr[v]);
+        else warp_add_term_digits(sdig + v * kDigits, rr[v]);
       }
     }
   };
