@@ -287,6 +287,14 @@ typedef struct {
   int err_kind;             /* out: 0 repro_sum non-finite, 1..5 compute_dt field p,u,v,w,T */
   double seconds;           /* out: device time of iterations first_it+1.. (iteration 1 excluded when first_it==1) */
   cav_ledger ledger;        /* in/out: accumulated */
+  /* Device-side convergence (single-rank blocks; ignored otherwise): with
+   * device_conv and want_norms, the run stops on the device after the first
+   * check iteration where max_v |R_v| / peak_v <= conv_tol (the rule of
+   * src/runner.cpp:210-220); no iteration after it is marched. */
+  int device_conv;          /* in: request; out: 1 if this block honoured it (else all n_its were marched) */
+  double conv_tol;          /* in */
+  double conv_peaks[5];     /* in/out: per-variable peak norms carried across calls */
+  long long conv_iter;      /* out: the converged iteration, 0 = not converged */
 } cav_run_io;
 
 /* Marches n_its iterations of rank_main's loop body (src/runner.cpp:184-235)

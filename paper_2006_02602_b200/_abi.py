@@ -103,7 +103,9 @@ class RunIO(C.Structure):
                 ("want_norms", C.c_int), ("norm_digits", C.POINTER(C.c_uint64)),
                 ("check_iters", C.POINTER(C.c_longlong)), ("n_checks", C.c_longlong),
                 ("err_iteration", C.c_longlong), ("err_kind", C.c_int),
-                ("seconds", C.c_double), ("ledger", Ledger)]
+                ("seconds", C.c_double), ("ledger", Ledger),
+                ("device_conv", C.c_int), ("conv_tol", C.c_double), ("conv_peaks", C.c_double * 5),
+                ("conv_iter", C.c_longlong)]
 
 
 def apply_overrides(cfg, **kw):

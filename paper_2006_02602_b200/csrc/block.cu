@@ -691,6 +691,32 @@ cudaEvent_t make_event() {
 
 }  // namespace
 
+// Device-side convergence decision (single-rank blocks): the rule of
+// src/runner.cpp:210-220 — per-variable peaks of the L2 residual norms, stop
+// at the first check where max_v |R_v| / peak_v <= conv_tol — evaluated on the
+// exact norm digits right after each check iteration, so a solve runs without
+// a host round trip per check. Later step kernels see `stop` and return.
+struct ConvState {
+  int stop;
+  int pad;
+  long long it;
+  double peaks[5];
+};
+
+__global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal) {
+  if (threadIdx.x != 0 || c->stop) return;
+  double worst = 0.0;
+  for (int v = 0; v < 5; ++v) {
+    const double l2 = sqrt_rn(repro_value_from_digits(dig + v * kDigits) / nglobal);  // norms_from_partials
+    c->peaks[v] = smax(c->peaks[v], l2);
+    if (c->peaks[v] > 0.0) worst = smax(worst, l2 / c->peaks[v]);
+  }
+  if (worst <= tol) {
+    c->stop = 1;
+    c->it = it;
+  }
+}
+
 // pcs_1 = p'(centre) of the first step (eager mode; later ones are folded by
 // the step kernel's last CTA).
 __global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, BetaFast bf,
@@ -801,6 +827,8 @@ struct Block {
   MsgDesc* d_unpack = nullptr;
   Slot** d_peer_slots = nullptr;
   unsigned long long* digits = nullptr;
+  ConvState* conv = nullptr;              // device convergence state (single rank)
+  const int* stop_flag = nullptr;         // = &conv->stop while a device-converging run is active
   long long digits_cap = 0;
   bool ready = false;
   long long next_n = 1;
@@ -906,6 +934,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_import));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_center_pcs));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_conv_check));
   }
   {
     const char* k = std::getenv("CAV_STEP_KERNEL");
@@ -942,6 +971,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaMalloc(&dbg, kDbgStages * sizeof(unsigned long long)));
   CAV_CUDA(cudaMemsetAsync(dbg, 0, kDbgStages * sizeof(unsigned long long), s0));
   CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
+  CAV_CUDA(cudaMalloc(&conv, sizeof(ConvState)));
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
   if (!plan.empty()) {
@@ -973,6 +1003,7 @@ Block::~Block() {
   cudaFree(sc);
   cudaFree(err);
   cudaFree(counters);
+  cudaFree(conv);
   cudaFree(dbg);
   cudaFree(d_peer_slots);
   cudaFree(d_pack);
@@ -1093,6 +1124,7 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.bf = bf;
     a.work = counters + 62;
     a.eager = eager ? 1 : 0;
+    a.stop = stop_flag;
     a.box = box;
     a.sc = sc + (it & 1);
     a.acc = acc + (it & 1);
@@ -1108,8 +1140,12 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.ntiles = a.tiles_x * ((bh + ty - 1) / ty);
     // k-chunk: long items amortise the per-item window restart (4 extra
     // planes); the dynamic counter balances them and the short tail chunks
-    // below trim the end (measured at 256^3: 48 best of 24..96, +0.6% over 32)
-    a.chunk = std::min(bd, 48);
+    // below trim the end (measured at 256^3: 48 best of 24..96, +0.6% over 32).
+    // Small boxes get shorter chunks so that there are items for every CTA
+    // (a 32^3 block has 4 tiles: 48-plane items would leave 292 CTAs idle).
+    a.chunk = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(48, static_cast<long long>(bd) * a.ntiles / tma_grid)));
+    a.chunk = std::min(a.chunk, bd);
     if (tma_chunk > 0) a.chunk = std::min(bd, tma_chunk);  // CAV_TMA_CHUNK (experiments)
     // tail: about two waves' worth of short items at the end of the order
     {
@@ -1306,10 +1342,6 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
   a.timeout_flag = tflag;
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
-  if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
-    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, sc + 1, cx, cy, cz);
-    CAV_CUDA(cudaGetLastError());
-  }
   cur ^= 1;
 }
 
@@ -1509,6 +1541,18 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
     if (!b.primed) b.prologue();
     if (mark) b.host_marks[2] = host_now();
+    // device convergence: single-rank fused pipeline only (other ranks' norm
+    // partials would have to be merged first; those runs fold on the host)
+    const bool dconv = io->device_conv && io->want_norms && b.d.np == 1 && b.use_tma && b.eager;
+    io->device_conv = dconv ? 1 : 0;
+    const int cur0 = b.cur;
+    if (dconv) {
+      ConvState c{};
+      for (int v = 0; v < 5; ++v) c.peaks[v] = io->conv_peaks[v];
+      CAV_CUDA(cudaMemcpyAsync(b.conv, &c, sizeof c, cudaMemcpyHostToDevice, b.s0));
+      b.stop_flag = &b.conv->stop;
+    }
+    const double nglobal = static_cast<double>(b.gn[0]) * b.gn[1] * b.gn[2];
     bool started = false;
     if (first != 1) {
       CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
@@ -1521,6 +1565,10 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       if (chk && io->check_iters) io->check_iters[ci] = it;
       ci += chk;
       b.iteration(it, chk, dig, false);
+      if (dconv && chk) {
+        k_conv_check<<<1, 32, 0, b.s0>>>(dig, b.conv, it, io->conv_tol, nglobal);
+        CAV_CUDA(cudaGetLastError());
+      }
       if (mark && it == 1) b.host_marks[3] = host_now();
       b.update_ledger(io->ledger);
       if (it == 1) {  // iteration 1 is warm-up (src/runner.cpp:186)
@@ -1537,6 +1585,21 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     io->seconds = ms * 1e-3;
     b.next_n = last + 1;
     io->n_checks = nchk;
+    io->conv_iter = 0;
+    if (dconv) {
+      b.stop_flag = nullptr;
+      ConvState c{};
+      CAV_CUDA(cudaMemcpy(&c, b.conv, sizeof c, cudaMemcpyDeviceToHost));
+      for (int v = 0; v < 5; ++v) io->conv_peaks[v] = c.peaks[v];
+      if (c.stop) {  // iterations after c.it returned at once: rewind the host's view
+        io->conv_iter = c.it;
+        b.next_n = c.it + 1;
+        b.cur = cur0 ^ static_cast<int>((c.it - first + 1) & 1);
+        long long kept = 0;
+        for (long long q = first; q <= c.it; ++q) kept += is_check(q);
+        io->n_checks = nchk = kept;
+      }
+    }
     if (nchk && io->norm_digits)
       CAV_CUDA(cudaMemcpyAsync(io->norm_digits, b.digits, nchk * 5 * kDigits * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, b.s0));

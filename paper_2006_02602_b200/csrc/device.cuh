@@ -266,6 +266,49 @@ __device__ __forceinline__ void add_term_digits(unsigned long long* dig, double 
   if (tp.c) atomicAdd(&dig[tp.d + 2], static_cast<unsigned long long>(tp.c));
 }
 
+// ---- exact norms on the device (single thread) -------------------------------
+// The host's digits_to_limbs + repro_value (host.cpp, ReproSum::value,
+// inc/util/repro_sum.hpp:48-77) for a positive accumulator: carry-save
+// radix-2^32 digits -> binary magnitude * 2^-1140, rounded to nearest even.
+// NaN on accumulator overflow (the host fold of the same digits throws).
+__device__ inline double repro_value_from_digits(const unsigned long long* dig) {
+  constexpr int kLimbs = 35;
+  unsigned long long mag[kLimbs];
+  unsigned __int128 carry = 0;
+  for (int l = 0; l < kLimbs; ++l) {
+    carry += dig[2 * l];
+    const unsigned long long lo = static_cast<unsigned long long>(carry) & 0xFFFFFFFFull;
+    carry >>= 32;
+    carry += dig[2 * l + 1];
+    const unsigned long long hi = static_cast<unsigned long long>(carry) & 0xFFFFFFFFull;
+    carry >>= 32;
+    mag[l] = lo | (hi << 32);
+  }
+  if (carry != 0) return __longlong_as_double(0x7FF8000000000000ll);
+  int top = -1;
+  for (int l = kLimbs - 1; l >= 0 && top < 0; --l)
+    if (mag[l]) top = l * 64 + 63 - __clzll(static_cast<long long>(mag[l]));
+  if (top < 0) return 0.0;
+  auto bit = [&](int x) { return static_cast<int>((mag[x >> 6] >> (x & 63)) & 1); };
+  const int lo = top <= 52 ? 0 : top - 52;
+  unsigned long long m = 0;
+  for (int x = top; x >= lo; --x) m = (m << 1) | static_cast<unsigned long long>(bit(x));
+  int e2 = -1140;
+  if (top > 52) {  // round to nearest, ties to even, with guard and sticky
+    const int gb = bit(top - 53);
+    bool sticky = false;
+    for (int x = top - 54; x >= 0 && !sticky; --x) sticky = bit(x) != 0;
+    if (gb && (sticky || (m & 1))) {
+      if (++m == (1ull << 53)) {
+        m >>= 1;
+        ++top;
+      }
+    }
+    e2 = top - 52 - 1140;
+  }
+  return ldexp(static_cast<double>(m), e2);
+}
+
 // ---- cross-GPU flag protocol (system scope: peers may be other GPUs) ----
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;

@@ -168,9 +168,18 @@ void rank_main(Shared& sh, int rank) {
   cav_run_io io{};
   double seconds = 0.0;
   long long it = 1;
+  // One rank: the convergence rule runs on the device after every check, so
+  // a segment can span many checks without a host round trip (the segment
+  // stops where the run converged). Several ranks: one check per segment,
+  // folded here across ranks.
+  bool dconv = !fixed && sh.np == 1;  // confirmed by the block after the first (1-iteration) segment
+  double conv_peaks[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   while (it <= target) {
     long long end = target;
-    if (!fixed) end = std::min(target, it == 1 ? 1 : (it + cadence - 1) / cadence * cadence);
+    if (!fixed) {
+      const long long span = dconv ? 256LL * cadence : cadence;
+      end = std::min(target, it == 1 ? 1 : (it + span - 1) / cadence * cadence);
+    }
     const long long nits = end - it + 1;
     long long nchk = 0;
     for (long long q = it; q <= end; ++q) nchk += norms && (q == 1 || q % cadence == 0);
@@ -183,7 +192,13 @@ void rank_main(Shared& sh, int rank) {
     io.want_norms = norms;
     io.norm_digits = dig.data();
     io.check_iters = citers.data();
+    io.device_conv = dconv ? 1 : 0;
+    io.conv_tol = cfg.conv_tol;
+    for (int v = 0; v < 5; ++v) io.conv_peaks[v] = conv_peaks[v];
     check(cav_block_run(b, &io));
+    dconv = dconv && io.device_conv;
+    for (int v = 0; v < 5; ++v) conv_peaks[v] = io.conv_peaks[v];
+    if (io.conv_iter) end = io.conv_iter;  // the device stopped there
     seconds += io.seconds;
     if (rank == 0) sh.check_iters = citers;
     sh.bar.wait();

@@ -117,6 +117,7 @@ struct TmaStepArgs {
   BetaFast bf;  // beta shortcuts (host::beta_fast)
   unsigned* work;  // dynamic item counter (items >= gridDim.x), reset by the last CTA
   int eager;      // store fl(p' - sc->pcs) and fold pcs_{n+1} (single rank); see IterScalars
+  const int* stop;  // device convergence: set once converged, later steps do nothing (or null)
   cav_box box;
   const IterScalars* sc;
   Acc* acc;
@@ -340,6 +341,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   long long* sitem = reinterpret_cast<long long*>(empty + R);  // item of each slot's entry (-1 = end)
   unsigned long long* sdig = reinterpret_cast<unsigned long long*>(sitem + R);
 
+  // the run converged at an earlier check (device decision): march no further
+  if (a.stop && *reinterpret_cast<const volatile int*>(a.stop)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {

@@ -260,3 +260,19 @@ def test_beta_branches_match_oracle(u_ref, np_):
     assert np.abs(o["fields"].reshape(5, -1)[1:4]).max() > u_ref  # the flow does outrun u_ref
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
     np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+
+
+def test_c0_solve_to_convergence_matches_oracle():
+    """`cavity solve`'s default mode on configs[0]'s grid: march until the
+    convergence rule holds (src/runner.cpp:210-220), decided on the device
+    after every check, no host round trip per check. Same converged
+    iteration (~6600, P/README.md:43-44), fields and norm history as the
+    oracle, bitwise."""
+    cfg = capi.default_config(grid=(32, 32, 32), steps=-1)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True)
+    o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
+    assert r.converged and o["converged"]
+    assert r.steps_marched == o["steps_marched"]
+    assert list(r.history_iter) == list(o["history_iter"])
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
