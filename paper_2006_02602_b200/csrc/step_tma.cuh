@@ -59,6 +59,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
 // the phase completes (or the hint elapses) instead of re-issuing the probe,
 // which keeps idle consumers off the issue slots.
+// Shared-window address forms: the consumer loop keeps the barrier arrays'
+// shared addresses in registers instead of converting generic pointers
+// (S2R of the CTA window + arithmetic) at every wait and release.
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITS:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITS;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -388,6 +405,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned nbad = 0;
   const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
   const double* ringq = ring + Cfg::PField + (ty + 1) * kQW + tx + 2;  // own u cell in slot 0
+  const uint32_t full_s = tma::smem_u32(full), empty_s = tma::smem_u32(empty);
   int sw = 0;  // slot of the next entry to wait for, and its phase
   uint32_t phw = 0;
   auto advance = [&](int& sl, uint32_t& ph) {
@@ -407,7 +425,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     bool any = false;
     for (int q = 0; q < count; ++q) {
       sl[q] = sw;
-      tma::mbar_wait(&full[sw], phw);
+      tma::mbar_wait_s(full_s + 8u * sw, phw);
       advance(sw, phw);
       any = any || plane_needs_rescale(a, pl + q, lazy);
     }
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   };
   auto release_slot = [&](int sl) {
     __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[sl]);
+    if (lane == 0) tma::mbar_arrive_s(empty_s + 8u * sl);
   };
   auto slot = [&](int sl) { return ringc + sl * kTmaSlot; };
   auto qslot = [&](int sl) { return ringq + sl * kTmaSlot; };
@@ -511,7 +529,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   };
 
   for (;;) {
-    tma::mbar_wait(&full[sw], phw);  // the next entry's item (re-waited below: completed phase)
+    tma::mbar_wait_s(full_s + 8u * sw, phw);  // the next entry's item (re-waited below: completed phase)
     const long long item = sitem[sw];
     if (item < 0) break;
     const ItemGeom it = item_geom<C>(a, item);
