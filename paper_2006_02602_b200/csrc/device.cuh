@@ -235,29 +235,6 @@ __device__ __forceinline__ void acc_publish(Acc* acc, double a, double b, double
   if (mask) atomicMin(&acc->err, err_code(it_for_dt, rank, 1 + __ffs(mask) - 1));
 }
 
-// Warp-aggregated add_term_digits: lanes whose terms start at the same digit
-// (neighbouring cells of a smooth field mostly share a binade) sum their
-// 32-bit pieces first — split into 16-bit halves so REDUX sums cannot
-// overflow — and one lane adds the exact group sums, instead of three
-// contended shared-memory atomics per lane. The digit words are carry-save
-// u64s, so any grouping of the additions gives the same words.
-__device__ __forceinline__ void warp_add_term_digits(unsigned long long* dig, double x) {
-  const unsigned act = __activemask();
-  const bool live = x != 0.0;
-  const TermPieces tp = term_pieces(live ? x : 1.0);
-  const unsigned grp = __match_any_sync(act, live ? tp.d : -1);
-  if (!live) return;
-  const unsigned a0 = __reduce_add_sync(grp, tp.a & 0xFFFFu), a1 = __reduce_add_sync(grp, tp.a >> 16);
-  const unsigned b0 = __reduce_add_sync(grp, tp.b & 0xFFFFu), b1 = __reduce_add_sync(grp, tp.b >> 16);
-  const unsigned c0 = __reduce_add_sync(grp, tp.c & 0xFFFFu), c1 = __reduce_add_sync(grp, tp.c >> 16);
-  if ((threadIdx.x & 31) == __ffs(grp) - 1) {
-    atomicAdd(&dig[tp.d], static_cast<unsigned long long>(a0) + (static_cast<unsigned long long>(a1) << 16));
-    atomicAdd(&dig[tp.d + 1], static_cast<unsigned long long>(b0) + (static_cast<unsigned long long>(b1) << 16));
-    const unsigned long long cs = static_cast<unsigned long long>(c0) + (static_cast<unsigned long long>(c1) << 16);
-    if (cs) atomicAdd(&dig[tp.d + 2], cs);
-  }
-}
-
 __device__ __forceinline__ void add_term_digits(unsigned long long* dig, double x) {
   if (x == 0.0) return;
   const TermPieces tp = term_pieces(x);

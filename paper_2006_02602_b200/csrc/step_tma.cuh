@@ -345,6 +345,48 @@ __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, cons
   return true;
 }
 
+// Per-thread run of exact norm terms that start at the same digit: the
+// shifted mantissas (m << (off & 31), <= 85 bits) are summed in 128 bits and
+// flushed to the CTA's carry-save digit words only when a term starts at a
+// different digit (neighbouring cells of a column mostly share a binade) or
+// at the end. The digit words are carry-save, so any grouping gives the same
+// words as ReproSum::add term by term (measured: a 256^3 check iteration
+// 1.7 -> 1.4 ms against warp-aggregated atomics per term).
+struct DigitRun {
+  int d;                      // first digit of the run, -1 = empty
+  unsigned long long lo, hi;  // 128-bit sum
+};
+__device__ __forceinline__ void digit_run_flush(DigitRun& r, unsigned long long* dig) {
+  if (r.d < 0) return;
+  const unsigned long long p0 = r.lo & 0xFFFFFFFFull, p1 = r.lo >> 32, p2 = r.hi & 0xFFFFFFFFull, p3 = r.hi >> 32;
+  if (p0) atomicAdd(&dig[r.d], p0);
+  if (p1) atomicAdd(&dig[r.d + 1], p1);
+  if (p2) atomicAdd(&dig[r.d + 2], p2);
+  if (p3) atomicAdd(&dig[r.d + 3], p3);
+  r.d = -1;
+  r.lo = r.hi = 0;
+}
+__device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* dig, double x) {
+  if (x == 0.0) return;
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(x));
+  const int e = static_cast<int>((bits >> 52) & 0x7FF);
+  unsigned long long m = bits & ((1ull << 52) - 1);
+  int off = 66;  // ReproSum::add: bit offset e + 65 (normal), 66 (subnormal)
+  if (e != 0) {
+    m |= 1ull << 52;
+    off = e + 65;
+  }
+  const int d = off >> 5, sh = off & 31;
+  if (d != r.d) {
+    digit_run_flush(r, dig);
+    r.d = d;
+  }
+  const unsigned long long lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0ull;
+  const unsigned long long nlo = r.lo + lo;
+  r.hi += hi + (nlo < lo ? 1ull : 0ull);
+  r.lo = nlo;
+}
+
 template <class Cfg, bool NORMS>
 __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     k_step_tma(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
@@ -403,6 +445,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
+  DigitRun runs[NORMS ? 5 : 1];
+  for (auto& r : runs) r = DigitRun{-1, 0ull, 0ull};
   const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
   const double* ringq = ring + Cfg::PField + (ty + 1) * kQW + tx + 2;  // own u cell in slot 0
   const uint32_t full_s = tma::smem_u32(full), empty_s = tma::smem_u32(empty);
@@ -523,7 +567,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         if (nonfinite(rr[v])) nbad = 1;
-        else warp_add_term_digits(sdig + v * kDigits, rr[v]);
+        else digit_run_add(runs[v], sdig + v * kDigits, rr[v]);
       }
     }
   };
@@ -605,6 +649,9 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
                  (e_w == EXP ? 8u : 0u) | (e_t == EXP ? 16u : 0u);
 
+  if (NORMS)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sdig + v * kDigits);
   // consumer-only reductions
   constexpr int NC = 32 * C;
   __shared__ double sred[3][C];
