@@ -771,27 +771,37 @@ using TmaV3 = TmaCfg<16, 8, 1>;
 constexpr int kTmaVariants = 4;
 constexpr int kTmaVariantTY[kTmaVariants] = {TmaV0::TY, TmaV1::TY, TmaV2::TY, TmaV3::TY};
 
+template <class Cfg, bool NORMS, bool G>
+void tma_attrs() {
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::Smem)));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  cudaFuncAttributes fa;
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, NORMS, G>));
+}
+
 template <class Cfg>
 int tma_setup(int device) {
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(Cfg::Smem)));
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(Cfg::Smem)));
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  cudaFuncAttributes fa;
-  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, false>));
-  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, true>));
+  tma_attrs<Cfg, false, false>();
+  tma_attrs<Cfg, true, false>();
+  tma_attrs<Cfg, false, true>();
+  tma_attrs<Cfg, true, true>();
   int per_sm = 0, sms = 0;
-  CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<Cfg, false>, Cfg::Threads, Cfg::Smem));
+  CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<Cfg, false, false>, Cfg::Threads,
+                                                         Cfg::Smem));
   CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   return std::max(1, std::min(per_sm, Cfg::CTAS)) * sms;
 }
 
 template <class Cfg>
-void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, int grid, cudaStream_t st) {
-  if (check) k_step_tma<Cfg, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
-  else k_step_tma<Cfg, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, int grid, cudaStream_t st) {
+  if (ghosts) {
+    if (check) k_step_tma<Cfg, true, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    else k_step_tma<Cfg, false, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+  } else {
+    if (check) k_step_tma<Cfg, true, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    else k_step_tma<Cfg, false, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+  }
   CAV_CUDA(cudaGetLastError());
 }
 
@@ -841,6 +851,9 @@ struct Block {
   CUtensorMap tmap[2][2];  // [state][p, uvwT]
   BetaFast bf{-1.0, 0u};
   bool eager = false;            // single-rank TMA pipeline: rescaled p stored directly
+  bool ghosts = false;           // eager pipeline with stored wall ghosts (see launch_step)
+  bool ghost_writes = true;     // CAV_GHOST_WRITES=0: always k_bc
+  bool step_wrote_ghosts = false;  // the last step kernel wrote its output's wall ghosts itself
   int tail_chunks = -1;          // CAV_TAIL_CHUNKS: short chunks at the end (-1 = two waves)
   int tma_chunk = 0;             // CAV_TMA_CHUNK: fixed k-chunk (0 = balanced choice)
   WallInfo winfo{};
@@ -943,6 +956,8 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     tma_chunk = getenv_int("CAV_TMA_CHUNK", 0);
     const char* ea = std::getenv("CAV_EAGER");
     eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
+    ghosts = eager && getenv_int("CAV_STORED_GHOSTS", 1) != 0;
+    ghost_writes = getenv_int("CAV_GHOST_WRITES", 1) != 0;
     const char* os = std::getenv("CAV_OVERLAP_STREAMS");
     two_streams = os && std::atoi(os) == 2;
     const char* v = std::getenv("CAV_TMA_CFG");
@@ -1105,6 +1120,10 @@ void Block::prologue() {
   a.timeout_flag = tflag;
   k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
+  if (ghosts) {  // the first input state's wall ghosts (stored-ghost step)
+    double* fc[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
+    ops::launch_bc(fc, g, walls, d.fluid, nullptr, s0);
+  }
   if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
     k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, sc + 1, cx, cy, cz);
     CAV_CUDA(cudaGetLastError());
@@ -1173,13 +1192,18 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.nu = d.fluid.nu;
     a.alpha = d.fluid.alpha;
     a.rescale = d.rescale;
+    // stored ghosts: the step writes its output's x-wall ghosts when the
+    // three interior layers next to each x wall lie in one warp (one 32-wide
+    // tile row); k_bc writes the remaining faces after it
+    a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
+    step_wrote_ghosts = a.gw != 0;
     const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
     const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
     switch (tma_variant) {
-      case 1: tma_launch<TmaV1>(tmap[cur], a, check, grid, s0); break;
-      case 2: tma_launch<TmaV2>(tmap[cur], a, check, grid, s0); break;
-      case 3: tma_launch<TmaV3>(tmap[cur], a, check, grid, s0); break;
-      default: tma_launch<TmaV0>(tmap[cur], a, check, grid, s0); break;
+      case 1: tma_launch<TmaV1>(tmap[cur], a, check, ghosts, grid, s0); break;
+      case 2: tma_launch<TmaV2>(tmap[cur], a, check, ghosts, grid, s0); break;
+      case 3: tma_launch<TmaV3>(tmap[cur], a, check, ghosts, grid, s0); break;
+      default: tma_launch<TmaV0>(tmap[cur], a, check, ghosts, grid, s0); break;
     }
     return;
   }
@@ -1317,6 +1341,11 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
     launch_shells(it, check, dig);
   }
   if (use_tma && d.np == 1) {  // the step kernel's last CTA folded the scalars
+    if (ghosts) {  // wall ghosts of the output state for the next step (eager: no pending shift)
+      double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
+      const int yz[6] = {0, 0, walls[2], walls[3], walls[4], walls[5]};
+      ops::launch_bc(fo, g, step_wrote_ghosts ? yz : walls, d.fluid, nullptr, s0, true);
+    }
     cur ^= 1;
     return;
   }

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kNormThreads) k_norm_digits(cav_field_ptrs f, 
 // kernel is order-free.
 struct BcArgs {
   double* f[5];
+  int step_only;  // 1: only the ghosts a step reads (u,v,w,T first layer)
   Geo g;
   int nfaces;
   int face[6];
@@ -190,16 +191,16 @@ __global__ void k_bc(BcArgs a) {
 #pragma unroll
   for (int v = 1; v <= 3; ++v) {  // no-slip: antisymmetric velocity
     a.f[v][cg0] = -a.f[v][ci0];
-    a.f[v][cg1] = -a.f[v][ci1];
+    if (!a.step_only) a.f[v][cg1] = -a.f[v][ci1];
   }
   double* T = a.f[4];
   if (ax == 0) {  // isothermal x walls
     const double tw = high ? a.t_cold : a.t_hot;
     T[cg0] = 2.0 * tw - T[ci0];
-    T[cg1] = 2.0 * tw - T[ci1];
+    if (!a.step_only) T[cg1] = 2.0 * tw - T[ci1];
   } else {  // adiabatic y/z walls
     T[cg0] = T[ci0];
-    T[cg1] = T[ci1];
+    if (!a.step_only) T[cg1] = T[ci1];
   }
   double* P = a.f[0];
   const double pc = a.sc ? a.sc->pc : 0.0;
@@ -214,8 +215,9 @@ __global__ void k_bc(BcArgs a) {
 namespace ops {
 
 void launch_bc(double* const fields[5], const Geo& g, const int walls[6], const cav_fluid_params& prm,
-               const IterScalars* sc, cudaStream_t st) {
+               const IterScalars* sc, cudaStream_t st, bool step_only) {
   BcArgs a{};
+  a.step_only = step_only ? 1 : 0;
   for (int v = 0; v < 5; ++v) a.f[v] = fields[v];
   a.g = g;
   a.t_hot = prm.t_hot;

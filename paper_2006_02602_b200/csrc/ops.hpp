@@ -17,7 +17,7 @@ void update_box(double* q, const double* r, double dt, int X, int Y, const cav_b
 // non-null the interior pressure read by the cubic extrapolation gets the
 // pending shift fl(p - sc->pc) (the lazy rescale).
 void launch_bc(double* const fields[5], const Geo& g, const int walls[6], const cav_fluid_params& prm,
-               const IterScalars* sc, cudaStream_t st);
+               const IterScalars* sc, cudaStream_t st, bool step_only = false);
 
 // compute_dt's scans (src/solver.cpp:200-227) over `box` of layout g in one
 // pass: CFL-denominator maxima and the non-finite mask, published into *acc

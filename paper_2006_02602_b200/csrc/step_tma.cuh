@@ -158,6 +158,11 @@ struct TmaStepArgs {
   unsigned long long* err_sticky;
   double dx, dy, dz, cfl, nu, alpha;
   int rescale;
+  // stored-ghost step (G): the lanes next to an x wall also store the x-wall
+  // ghosts of the output state, from their neighbours' new values (shuffles;
+  // the three interior layers lie in one warp: checked on the host); k_bc
+  // writes the y and z faces. 0: k_bc writes every face.
+  int gw;
 };
 
 struct ItemGeom {
@@ -387,7 +392,13 @@ __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* d
   r.lo = nlo;
 }
 
-template <class Cfg, bool NORMS>
+// G (stored wall ghosts, single rank): every wall ghost the step reads is
+// already in the input state (x walls: stored by the previous step's wall
+// lanes, a.gw; y/z walls: k_bc after it), so the consumers take the plain
+// accessor everywhere. Without G they are formed in registers (x/y:
+// SmemAcc<.., true>, z: the p window rules below); the three accessor
+// instances cost 16% at 256^3 even though few warps take the wall paths.
+template <class Cfg, bool NORMS, bool G>
 __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     k_step_tma(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
                const TmaStepArgs a) {
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // slm, slk, slp hold planes kk-1, kk, kk+1.
   auto cell = [&](int slm, int slk, int slp, int kk, double p0, double pzm, double pzp, double pzm2, double pzp2,
                   double* op, bool ccolk) {
-    const int zf = (zlo && kk == 2 ? kZlo2 : 0) | (zhi && kk == g.nz + 1 ? kZhi1 : 0);
+    const int zf = G ? 0 : (zlo && kk == 2 ? kZlo2 : 0) | (zhi && kk == g.nz + 1 ? kZhi1 : 0);
     Res r;
     double uc, vc, wc, tc;
     // warp-uniform path choice: plain, x walls only (the x-wall tile columns),
@@ -539,8 +550,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     wc = sa.w();                                                                                            \
     tc = sa.t();                                                                                            \
   }
-    if (wyz || zf) CAV_RES(true, true)
-    else if (wx) CAV_RES(true, false)
+    if (!G && (wyz || zf)) CAV_RES(true, true)
+    else if (!G && wx) CAV_RES(true, false)
     else CAV_RES(false, false)
 #undef CAV_RES
     const double qpp = p0 + dt * r.p, qpn = qpp - pcs, qun = uc + dt * r.u, qvn = vc + dt * r.v, qwn = wc + dt * r.w,
@@ -552,6 +563,24 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     __stcs(op + 2 * fs, qvn);
     __stcs(op + 3 * fs, qwn);
     __stcs(op + 4 * fs, qtn);
+    if (G && (wfl & 4)) {  // x-wall ghosts of the output (k_bc's expressions), from the neighbours' p
+      const unsigned am = __activemask();
+      const double pu1 = __shfl_down_sync(am, qpn, 1), pu2 = __shfl_down_sync(am, qpn, 2);
+      const double pd1 = __shfl_up_sync(am, qpn, 1), pd2 = __shfl_up_sync(am, qpn, 2);
+      if (wfl & 3) {
+        const bool h = (wfl & 2) != 0;
+        const int sg = h ? 1 : -1;
+        const double q1 = h ? pd1 : pu1, q2 = h ? pd2 : pu2;
+        const double pg0 = cubic_g0(qpn, q1, q2);
+        // explicit global stores (see above)
+        __stcs(op + sg, pg0);
+        __stcs(op + 2 * sg, cubic_g1(pg0, qpn, q1));
+        __stcs(op + fs + sg, -qun);
+        __stcs(op + 2 * fs + sg, -qvn);
+        __stcs(op + 3 * fs + sg, -qwn);
+        __stcs(op + 4 * fs + sg, 2.0 * (h ? a.walls.t_cold : a.walls.t_hot) - qtn);
+      }
+    }
     const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, a.bf);
     m0 = dmax_d(m0, d.du);
     m1 = dmax_d(m1, d.dv);
@@ -582,7 +611,12 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
     const bool ccol = i == a.cx && j == a.cy;
     // x/y walls next to this thread's column: register ghosts (SmemAcc<.., true>)
-    {
+    if (G && a.gw) {  // wfl (G): 1 = i == 2 at the low x wall, 2 = i == nx+1 at the high one, 4 = in this warp
+      const int xl = a.walls.wall[0] && i == 2, xh = a.walls.wall[1] && i == g.nx + 1;
+      wfl = active ? (xl | (xh << 1)) : 0;
+      if (__any_sync(0xffffffffu, wfl != 0)) wfl |= 4;
+    }
+    if (!G) {
       const WallInfo& w = a.walls;
       wfl = (w.wall[0] && i == 2 ? kXlo2 : 0) | (w.wall[0] && i == 3 ? kXlo3 : 0) |
             (w.wall[1] && i == g.nx + 1 ? kXhi1 : 0) | (w.wall[1] && i == g.nx ? kXhi0 : 0) |
@@ -615,8 +649,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       int sn[2];
       wait_planes(it, k + 2, 1, sn);
       P[4] = slot(sn[0])[0];
-      const bool zh5 = zhi && k + 3 >= g.nz + 2;
-      if ((zlo && k <= 3) || zh5) zwall2(P, k);
+      const bool zh5 = !G && zhi && k + 3 >= g.nz + 2;
+      if (!G && ((zlo && k <= 3) || zh5)) zwall2(P, k);
       if (active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
       wait_planes(it, k + 3, 1, sn + 1);
       if (!zh5) P[5] = slot(sn[1])[0];
@@ -636,7 +670,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       int sn[2];
       wait_planes(it, k + 2, 1, sn);  // plane k+2
       P[4] = slot(sn[0])[0];
-      if ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2)) zwall1(P, k);
+      if (!G && ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2))) zwall1(P, k);
       if (active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
       release_slot(sn[0]);
     }

@@ -276,3 +276,26 @@ def test_c0_solve_to_convergence_matches_oracle():
     assert list(r.history_iter) == list(o["history_iter"])
     np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+
+
+@pytest.mark.parametrize("env", [{}, {"CAV_GHOST_WRITES": "0"}, {"CAV_STORED_GHOSTS": "0"}])
+@pytest.mark.parametrize("n", [(67, 19, 11), (33, 9, 7), (34, 12, 5), (64, 8, 6)])
+def test_stored_wall_ghosts_match_oracle(monkeypatch, env, n):
+    """Single-rank steps with the wall ghosts stored in the state (x walls by
+    the step kernel's wall lanes when three interior layers share a warp, the
+    rest by k_bc), with k_bc only, and with register ghosts: all bitwise equal
+    to the oracle, ghost cells included (block API, arbitrary state)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    f = O.random_fields(n, 7 + n[0], vel=0.03)
+    f[0] *= 1e-3
+    b = capi.Block(0, 1, n, (1, 1, 1))
+    b.upload(f)
+    b.run(5)
+    h = capi.cavity_spacing(n)
+    want = O.march(f, n, h, capi.fluid_for_rayleigh(1e5), 0.4, 5)
+    np.testing.assert_array_equal(bits(b.download()), bits(want))
+    b.run(2)
+    want = O.march(want, n, h, capi.fluid_for_rayleigh(1e5), 0.4, 2)
+    np.testing.assert_array_equal(bits(b.download()), bits(want))
+    b.close()
