@@ -1678,7 +1678,8 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   (void)check;
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
-  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (b.use_tma && b.d.np == 1 ? 0 : 1);  // [bc], step, [sync]
+  // [bc before the v1 step], step, [bc after the stored-ghost step], [sync]
+  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (walls && b.ghosts ? 1 : 0) + (b.use_tma && b.d.np == 1 ? 0 : 1);
   if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);  // pack, wait, unpack, [shells]
   return n;
 }
