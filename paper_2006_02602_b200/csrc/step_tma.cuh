@@ -351,25 +351,25 @@ __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, cons
 }
 
 // Per-thread run of exact norm terms that start at the same digit: the
-// shifted mantissas (m << (off & 31), <= 85 bits) are summed in 128 bits and
-// flushed to the CTA's carry-save digit words only when a term starts at a
-// different digit (neighbouring cells of a column mostly share a binade) or
-// at the end. The digit words are carry-save, so any grouping gives the same
-// words as ReproSum::add term by term (measured: a 256^3 check iteration
-// 1.7 -> 1.4 ms against warp-aggregated atomics per term).
+// shifted mantissas (m << (off & 31), < 2^85) are summed in 96 bits and
+// flushed to the CTA's carry-save digit words when a term starts at a
+// different digit (neighbouring cells of a column mostly share a binade), at
+// the end of each item (at most 48 terms per run, so 96 bits cannot
+// overflow) and at the end. The digit words are carry-save, so any grouping
+// gives the same words as ReproSum::add term by term (measured: a 256^3 check
+// iteration 1.7 -> 1.4 ms against warp-aggregated atomics per term; 96 rather
+// than 128 bits frees 5 registers).
 struct DigitRun {
-  int d;                      // first digit of the run, -1 = empty
-  unsigned long long lo, hi;  // 128-bit sum
+  int d;                // first digit of the run, -1 = empty
+  unsigned w0, w1, w2;  // 96-bit sum
 };
 __device__ __forceinline__ void digit_run_flush(DigitRun& r, unsigned long long* dig) {
   if (r.d < 0) return;
-  const unsigned long long p0 = r.lo & 0xFFFFFFFFull, p1 = r.lo >> 32, p2 = r.hi & 0xFFFFFFFFull, p3 = r.hi >> 32;
-  if (p0) atomicAdd(&dig[r.d], p0);
-  if (p1) atomicAdd(&dig[r.d + 1], p1);
-  if (p2) atomicAdd(&dig[r.d + 2], p2);
-  if (p3) atomicAdd(&dig[r.d + 3], p3);
+  if (r.w0) atomicAdd(&dig[r.d], static_cast<unsigned long long>(r.w0));
+  if (r.w1) atomicAdd(&dig[r.d + 1], static_cast<unsigned long long>(r.w1));
+  if (r.w2) atomicAdd(&dig[r.d + 2], static_cast<unsigned long long>(r.w2));
   r.d = -1;
-  r.lo = r.hi = 0;
+  r.w0 = r.w1 = r.w2 = 0u;
 }
 __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* dig, double x) {
   if (x == 0.0) return;
@@ -386,10 +386,11 @@ __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* d
     digit_run_flush(r, dig);
     r.d = d;
   }
-  const unsigned long long lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0ull;
-  const unsigned long long nlo = r.lo + lo;
-  r.hi += hi + (nlo < lo ? 1ull : 0ull);
-  r.lo = nlo;
+  const unsigned long long lo = m << sh;
+  const unsigned hi = sh ? static_cast<unsigned>(m >> (64 - sh)) : 0u;
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(r.w0), "+r"(r.w1), "+r"(r.w2)
+      : "r"(static_cast<unsigned>(lo)), "r"(static_cast<unsigned>(lo >> 32)), "r"(hi));
 }
 
 // G (stored wall ghosts, single rank): every wall ghost the step reads is
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
   DigitRun runs[NORMS ? 5 : 1];
-  for (auto& r : runs) r = DigitRun{-1, 0ull, 0ull};
+  for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
   const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
   const double* ringq = ring + Cfg::PField + (ty + 1) * kQW + tx + 2;  // own u cell in slot 0
   const uint32_t full_s = tma::smem_u32(full), empty_s = tma::smem_u32(empty);
@@ -688,6 +689,9 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     release_slot(skm);
     release_slot(sk0);
     release_slot(sk1);
+    if (NORMS)  // bounds every run to one item's planes (96-bit sums)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sdig + v * kDigits);
   }
   constexpr unsigned EXP = 0x7FF00000u;
   unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
