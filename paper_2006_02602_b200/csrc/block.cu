@@ -956,7 +956,11 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     tma_chunk = getenv_int("CAV_TMA_CHUNK", 0);
     const char* ea = std::getenv("CAV_EAGER");
     eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
-    ghosts = eager && getenv_int("CAV_STORED_GHOSTS", 1) != 0;
+    // stored ghosts pay from about 150^3 (measured per iteration: 32^3 14.6
+    // vs 10.3 us, 128^3 62.1 vs 60.7 us, 256^3 321 vs 335 us): below that the
+    // extra k_bc launch costs more than the single accessor saves
+    const int sg = getenv_int("CAV_STORED_GHOSTS", -1);
+    ghosts = eager && (sg == 1 || (sg < 0 && static_cast<long long>(n[0]) * n[1] * n[2] >= 3000000LL));
     ghost_writes = getenv_int("CAV_GHOST_WRITES", 1) != 0;
     const char* os = std::getenv("CAV_OVERLAP_STREAMS");
     two_streams = os && std::atoi(os) == 2;

@@ -278,7 +278,8 @@ def test_c0_solve_to_convergence_matches_oracle():
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
 
 
-@pytest.mark.parametrize("env", [{}, {"CAV_GHOST_WRITES": "0"}, {"CAV_STORED_GHOSTS": "0"}])
+@pytest.mark.parametrize("env", [{"CAV_STORED_GHOSTS": "1"}, {"CAV_STORED_GHOSTS": "1", "CAV_GHOST_WRITES": "0"},
+                                 {"CAV_STORED_GHOSTS": "0"}])
 @pytest.mark.parametrize("n", [(67, 19, 11), (33, 9, 7), (34, 12, 5), (64, 8, 6)])
 def test_stored_wall_ghosts_match_oracle(monkeypatch, env, n):
     """Single-rank steps with the wall ghosts stored in the state (x walls by
