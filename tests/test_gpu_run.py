@@ -300,3 +300,16 @@ def test_stored_wall_ghosts_match_oracle(monkeypatch, env, n):
     want = O.march(want, n, h, capi.fluid_for_rayleigh(1e5), 0.4, 2)
     np.testing.assert_array_equal(bits(b.download()), bits(want))
     b.close()
+
+
+@pytest.mark.parametrize("grid", [(24, 20, 16), (37, 21, 13)])
+def test_stored_ghosts_norm_history_matches_oracle(monkeypatch, grid):
+    """The stored-ghost step (forced on below its size threshold) with norm
+    iterations every 5th step and a developed flow: fields and the residual
+    norm history bitwise equal to the oracle."""
+    monkeypatch.setenv("CAV_STORED_GHOSTS", "1")
+    cfg = capi.default_config(grid=grid, steps=80, check_every=5, u_ref=1e-3)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True)
+    o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
