@@ -42,7 +42,11 @@ def draw(seed):
 
 
 @pytest.mark.parametrize("seed", list(range(48)))
-def test_random_configuration_matches_oracle(seed):
+@pytest.mark.parametrize("ghosts", ["auto", "1"])
+def test_random_configuration_matches_oracle(monkeypatch, seed, ghosts):
+    """ghosts "1" forces the stored-wall-ghost step on every single-rank
+    draw (by default it starts at 3e6 cells, above these grids)."""
+    monkeypatch.setenv("CAV_STORED_GHOSTS", "1" if ghosts == "1" else "-1")
     kw = draw(seed)
     r = capi.run_case(capi.default_config(**kw), collect_fields=True, collect_history=True)
     serial = {k: v for k, v in kw.items() if k not in ("np", "mode", "strategy", "overlap")}
