@@ -572,12 +572,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
     if (G && (wfl & 4)) {  // x-wall ghosts of the output (k_bc's expressions), from the neighbours' p
       const unsigned am = __activemask();
-      const double pu1 = __shfl_down_sync(am, qpn, 1), pu2 = __shfl_down_sync(am, qpn, 2);
-      const double pd1 = __shfl_up_sync(am, qpn, 1), pd2 = __shfl_up_sync(am, qpn, 2);
+      const bool h = (wfl & 2) != 0;
+      const int sg = h ? 1 : -1;  // towards the wall
+      const double q1 = __shfl_sync(am, qpn, tx - sg), q2 = __shfl_sync(am, qpn, tx - 2 * sg);
       if (wfl & 3) {
-        const bool h = (wfl & 2) != 0;
-        const int sg = h ? 1 : -1;
-        const double q1 = h ? pd1 : pu1, q2 = h ? pd2 : pu2;
         const double pg0 = cubic_g0(qpn, q1, q2);
         // explicit global stores (see above)
         __stcs(op + sg, pg0);
