@@ -703,6 +703,61 @@ struct ConvState {
   double peaks[5];
 };
 
+// Exact residual-norm digits of a stored-ghost norm iteration: the squares of
+// the residuals k_step_tma<.., NORMS, G> left in the scratch state, summed into
+// the iteration's carry-save digits as the step's own digit runs would
+// (ReproSum, inc/util/repro_sum.hpp; residual_norm_partials,
+// src/solver.cpp:259-274). Each thread walks one k-segment of one (i,j)
+// column (coalesced across a warp), so its consecutive terms are z-neighbours
+// and the runs stay long, as in the step kernel.
+constexpr int kNormRunThreads = 256, kNormRunSeg = 64;
+__global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs, Geo g, cav_box b,
+                                                               unsigned long long* dig,
+                                                               unsigned long long* err_sticky, long long n,
+                                                               int rank) {
+  __shared__ unsigned long long sd[5 * kDigits];
+  for (int x = threadIdx.x; x < 5 * kDigits; x += kNormRunThreads) sd[x] = 0;
+  __syncthreads();
+  const int bw = b.hi[0] - b.lo[0], bh = b.hi[1] - b.lo[1];
+  const long long col = static_cast<long long>(blockIdx.x) * kNormRunThreads + threadIdx.x;
+  const int i = b.lo[0] + static_cast<int>(col % bw), j = b.lo[1] + static_cast<int>((col / bw) % bh);
+  const int k0 = b.lo[2] + static_cast<int>(col / (static_cast<long long>(bw) * bh)) * kNormRunSeg;
+  unsigned nf = 0;
+  if (col < static_cast<long long>(bw) * bh * ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg)) {
+    DigitRun runs[5];
+    for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
+    const long long fs = g.fstride, plane = static_cast<long long>(g.pitch) * g.ypitch;
+    const int k1 = min(k0 + kNormRunSeg, b.hi[2]);
+    const double* q = rs + g.idx(i, j, k0);
+    for (int k = k0; k < k1; ++k, q += plane) {
+      double x[5];
+#pragma unroll
+      for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + v * fs);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        const double x2 = x[v] * x[v];
+        if (nonfinite(x2)) nf = 1;
+        else digit_run_add(runs[v], sd + v * kDigits, x2);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sd + v * kDigits);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < 5 * kDigits; x += kNormRunThreads)
+    if (sd[x]) atomicAdd(&dig[x], sd[x]);
+  if (nf) atomicMin(err_sticky, err_code(n, rank, 0));  // the step kernel's non-finite norm error
+}
+
+void launch_norm_runs(const double* rs, const Geo& g, const cav_box& b, unsigned long long* dig,
+                      unsigned long long* err, long long n, int rank, cudaStream_t st) {
+  const long long cols = static_cast<long long>(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) *
+                         ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg);
+  k_norm_runs<<<static_cast<unsigned>((cols + kNormRunThreads - 1) / kNormRunThreads), kNormRunThreads, 0, st>>>(
+      rs, g, b, dig, err, n, rank);
+  CAV_CUDA(cudaGetLastError());
+}
+
 __global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal) {
   if (threadIdx.x != 0 || c->stop) return;
   double worst = 0.0;
@@ -818,6 +873,8 @@ struct Block {
   Geo g{};
   double* state[2]{};
   double* staging = nullptr;  // 5 * S doubles in the host Field3 layout (upload / download)
+  double* rscratch = nullptr;  // stored-ghost norm iterations: residuals (state layout), allocated on first use
+  bool step_used_scratch = false;  // the last step kernel left its residuals in rscratch
   int cur = 0;
   std::vector<cav_plan_entry> plan;
   ArenaLayout lay;
@@ -1017,6 +1074,7 @@ Block::~Block() {
   cudaFree(state[0]);
   cudaFree(state[1]);
   cudaFree(staging);
+  cudaFree(rscratch);
   cudaFree(arena);
   cudaFree(acc);
   cudaFree(sc);
@@ -1136,6 +1194,7 @@ void Block::prologue() {
 }
 
 void Block::launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig) {
+  step_used_scratch = false;
   const long long vol = host::box_volume(box);
   if (vol == 0) return;
   // TMA boxes must start 16-byte aligned along x (even FP64 element)
@@ -1200,6 +1259,11 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     // three interior layers next to each x wall lie in one warp (one 32-wide
     // tile row); k_bc writes the remaining faces after it
     a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
+    if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
+      if (!rscratch) CAV_CUDA(cudaMalloc(&rscratch, 5 * static_cast<size_t>(g.fstride) * sizeof(double)));
+      a.rs = rscratch;
+      step_used_scratch = true;
+    }
     step_wrote_ghosts = a.gw != 0;
     const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
     const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
@@ -1293,6 +1357,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
     if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
     launch_step(ib, it, check, dig);
     if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
+    if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, s0);
   } else if (!d.overlap) {
     x.msg = d_pack;
     k_pack<<<xgrid, kXThreads, 0, s0>>>(x);
@@ -1679,11 +1744,11 @@ int cav_block_debug(cav_block* bh, uint64_t* out, int cap) {
 
 int cav_block_launches_per_iteration(cav_block* bh, int check) {
   Block& b = *bh->b;
-  (void)check;
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
   // [bc before the v1 step], step, [bc after the stored-ghost step], [sync]
-  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (walls && b.ghosts ? 1 : 0) + (b.use_tma && b.d.np == 1 ? 0 : 1);
+  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (walls && b.ghosts ? 1 : 0) + (b.use_tma && b.d.np == 1 ? 0 : 1) +
+          (check && b.ghosts ? 1 : 0);  // [k_norm_runs]
   if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);  // pack, wait, unpack, [shells]
   return n;
 }

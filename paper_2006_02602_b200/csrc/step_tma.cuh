@@ -163,6 +163,10 @@ struct TmaStepArgs {
   // the three interior layers lie in one warp: checked on the host); k_bc
   // writes the y and z faces. 0: k_bc writes every face.
   int gw;
+  // G norm iterations: the residuals go to this scratch state (same layout)
+  // and k_norm_runs sums their squares after the step (the step's own digit
+  // runs need 5 x 4 more live registers and spill at 96)
+  double* rs;
 };
 
 struct ItemGeom {
@@ -457,7 +461,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
-  DigitRun runs[NORMS ? 5 : 1];
+  DigitRun runs[NORMS && !G ? 5 : 1];
+  const long long rdelta = NORMS && G ? a.rs - a.out : 0;
   for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
   const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
   const double* ringq = ring + Cfg::PField + (ty + 1) * kQW + tx + 2;  // own u cell in slot 0
@@ -599,7 +604,15 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     }
     // pc_n for the lazy shift (eager blocks fold pcs with center_p_update)
     if (!G && ccolk) a.acc->pc_local = qpp;
-    if (NORMS && (!G || live)) {
+    if (NORMS && G && live) {
+      double* rp = op + rdelta;
+      __stcs(rp, r.p);
+      __stcs(rp + fs, r.u);
+      __stcs(rp + 2 * fs, r.v);
+      __stcs(rp + 3 * fs, r.w);
+      __stcs(rp + 4 * fs, r.t);
+    }
+    if (NORMS && !G) {
       const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
@@ -687,7 +700,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     release_slot(skm);
     release_slot(sk0);
     release_slot(sk1);
-    if (NORMS)  // bounds every run to one item's planes (96-bit sums)
+    if (NORMS && !G)  // bounds every run to one item's planes (96-bit sums)
 #pragma unroll
       for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sdig + v * kDigits);
   }
@@ -695,7 +708,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned bad = (e_p == EXP ? 1u : 0u) | (e_u == EXP ? 2u : 0u) | (e_v == EXP ? 4u : 0u) |
                  (e_w == EXP ? 8u : 0u) | (e_t == EXP ? 16u : 0u);
 
-  if (NORMS)
+  if (NORMS && !G)
 #pragma unroll
     for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sdig + v * kDigits);
   // consumer-only reductions
@@ -757,7 +770,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       *a.done = 0;
     }
   }
-  if (NORMS)
+  if (NORMS && !G)
     for (int x = threadIdx.x; x < 5 * kDigits; x += NC)
       if (sdig[x]) atomicAdd(&a.digits[x], sdig[x]);
 }
