@@ -710,7 +710,7 @@ struct ConvState {
 // src/solver.cpp:259-274). Each thread walks one k-segment of one (i,j)
 // column (coalesced across a warp), so its consecutive terms are z-neighbours
 // and the runs stay long, as in the step kernel.
-constexpr int kNormRunThreads = 256, kNormRunSeg = 64;
+constexpr int kNormRunThreads = 256, kNormRunSeg = 128;
 __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs, Geo g, cav_box b,
                                                                unsigned long long* dig,
                                                                unsigned long long* err_sticky, long long n,
