@@ -758,6 +758,37 @@ void launch_norm_runs(const double* rs, const Geo& g, const cav_box& b, unsigned
   CAV_CUDA(cudaGetLastError());
 }
 
+// The y and z wall ghosts a stored-ghost step reads (p both layers, u,v,w,T
+// the first), of a single-rank state after a step whose wall lanes stored the
+// x ghosts: k_bc's expressions (apply_boundary_conditions, src/solver.cpp:
+// 158-191) with no pending shift. One block row per (face, transverse index),
+// threads along i: coalesced rows, no face search or 64-bit division.
+constexpr int kGhostThreads = 128;
+__global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz(double* s, Geo g, WallInfo w) {
+  const int face = 2 + static_cast<int>(blockIdx.z);
+  if (!w.wall[face]) return;
+  const int ax = face >> 1, hi = face & 1;
+  const int nn = ax == 1 ? g.ny : g.nz, nt = ax == 1 ? g.nz : g.ny;
+  if (static_cast<int>(blockIdx.y) >= nt) return;
+  const int t = 2 + static_cast<int>(blockIdx.y);  // k on a y face, j on a z face
+  const int c0 = hi ? nn + 1 : 2, c1 = hi ? nn : 3, c2 = hi ? nn - 1 : 4, g0 = hi ? nn + 2 : 1, g1 = hi ? nn + 3 : 0;
+  const long long fs = g.fstride;
+  for (int i = 2 + static_cast<int>(blockIdx.x) * kGhostThreads + static_cast<int>(threadIdx.x); i < g.nx + 2;
+       i += static_cast<int>(gridDim.x) * kGhostThreads) {
+    auto at = [&](int nrm) { return ax == 1 ? g.idx(i, nrm, t) : g.idx(i, t, nrm); };
+    const long long e0 = at(c0), q0 = at(g0);
+    const double p0 = s[e0], p1 = s[at(c1)], p2 = s[at(c2)];
+    const double u = s[fs + e0], v = s[2 * fs + e0], wv = s[3 * fs + e0], tt = s[4 * fs + e0];
+    const double pg0 = cubic_g0(p0, p1, p2);
+    s[q0] = pg0;
+    s[at(g1)] = cubic_g1(pg0, p0, p1);
+    s[fs + q0] = -u;  // no-slip: antisymmetric velocity
+    s[2 * fs + q0] = -v;
+    s[3 * fs + q0] = -wv;
+    s[4 * fs + q0] = tt;  // adiabatic
+  }
+}
+
 __global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal) {
   if (threadIdx.x != 0 || c->stop) return;
   double worst = 0.0;
@@ -1412,8 +1443,13 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, bool ti
   if (use_tma && d.np == 1) {  // the step kernel's last CTA folded the scalars
     if (ghosts) {  // wall ghosts of the output state for the next step (eager: no pending shift)
       double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
-      const int yz[6] = {0, 0, walls[2], walls[3], walls[4], walls[5]};
-      ops::launch_bc(fo, g, step_wrote_ghosts ? yz : walls, d.fluid, nullptr, s0, true);
+      if (step_wrote_ghosts) {
+        const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
+        k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo);
+        CAV_CUDA(cudaGetLastError());
+      } else {
+        ops::launch_bc(fo, g, walls, d.fluid, nullptr, s0, true);
+      }
     }
     cur ^= 1;
     return;
