@@ -1046,7 +1046,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
     // stored ghosts pay from about 150^3 (measured per iteration: 32^3 14.6
     // vs 10.3 us, 128^3 62.1 vs 60.7 us, 256^3 321 vs 335 us): below that the
-    // extra k_bc launch costs more than the single accessor saves
+    // extra ghost-kernel launch costs more than the single accessor saves
     const int sg = getenv_int("CAV_STORED_GHOSTS", -1);
     ghosts = eager && (sg == 1 || (sg < 0 && static_cast<long long>(n[0]) * n[1] * n[2] >= 3000000LL));
     ghost_writes = getenv_int("CAV_GHOST_WRITES", 1) != 0;
@@ -1288,7 +1288,7 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
     a.rescale = d.rescale;
     // stored ghosts: the step writes its output's x-wall ghosts when the
     // three interior layers next to each x wall lie in one warp (one 32-wide
-    // tile row); k_bc writes the remaining faces after it
+    // tile row); k_ghosts_yz writes the y and z faces after it (k_bc all faces otherwise)
     a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
     if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
       if (!rscratch) CAV_CUDA(cudaMalloc(&rscratch, 5 * static_cast<size_t>(g.fstride) * sizeof(double)));

@@ -160,8 +160,8 @@ struct TmaStepArgs {
   int rescale;
   // stored-ghost step (G): the lanes next to an x wall also store the x-wall
   // ghosts of the output state, from their neighbours' new values (shuffles;
-  // the three interior layers lie in one warp: checked on the host); k_bc
-  // writes the y and z faces. 0: k_bc writes every face.
+  // the three interior layers lie in one warp: checked on the host); k_ghosts_yz
+  // writes the y and z faces. 0: k_bc writes every face (block.cu).
   int gw;
   // G norm iterations: the residuals go to this scratch state (same layout)
   // and k_norm_runs sums their squares after the step (the step's own digit
@@ -399,7 +399,7 @@ __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* d
 
 // G (stored wall ghosts, single rank): every wall ghost the step reads is
 // already in the input state (x walls: stored by the previous step's wall
-// lanes, a.gw; y/z walls: k_bc after it), so the consumers take the plain
+// lanes, a.gw; y/z walls: k_ghosts_yz after it), so the consumers take the plain
 // accessor everywhere. Without G they are formed in registers (x/y:
 // SmemAcc<.., true>, z: the p window rules below); the three accessor
 // instances cost 16% at 256^3 even though few warps take the wall paths.
