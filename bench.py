@@ -58,10 +58,24 @@ def parse():
     return p.parse_args()
 
 
-def grid_of(args, n):
-    from paper_2006_02602_b200 import capi
+MODES = {"1d-i": 0, "1d-j": 1, "1d-k": 2, "2d": 3, "3d": 4}  # include/cavity_b200.h CAV_MODE_*
+
+
+def grid_of(args, n, reference=False):
+    """The workload grid: configs[1]'s 256^3 at N=1; for N>1 weak scaling the
+    reference's grow_grid type 2 (C4), strong scaling the grid as given.
+    reference=True asks the unmodified reference (oracle/_ref) instead of our
+    library, so the reference arm never loads libcavity_b200.so."""
     base = tuple(args.grid * 3)[:3] if len(args.grid) == 1 else tuple(args.grid)
     if args.scaling == "weak" and n > 1:
+        if reference:
+            import ctypes as C
+            from oracle.refbind import Ref
+            out = (C.c_int * 3)()
+            if Ref.lib().ref_grow_grid(base[0], base[1], base[2], n, MODES[args.mode], 2, out) != 0:
+                raise SystemExit("ref_grow_grid: " + Ref.lib().ref_last_error().decode())
+            return tuple(out)
+        from paper_2006_02602_b200 import capi
         return tuple(capi.grow_grid(base, n, args.mode, 2))
     return base
 
@@ -144,22 +158,31 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def ref_decomposition(grid, mode, max_np):
+    """Largest np <= max_np whose choose_dims/partition the reference itself
+    accepts for `grid` (src/decomp.cpp:67-150), and its dims."""
+    import ctypes as C
+    from oracle.refbind import Ref
+    L = Ref.lib()
+    for np_ in range(max(1, max_np), 0, -1):
+        dims = (C.c_int * 3)()
+        if L.ref_choose_dims(np_, MODES[mode], dims) != 0:
+            continue
+        ext = (C.c_int * (6 * np_))()
+        if L.ref_partition(grid[0], grid[1], grid[2], dims, ext) == 0:
+            return np_, tuple(dims)
+    return 1, (1, 1, 1)
+
+
 def cpu_reference(grid, seconds_budget, mode="3d", strategy="v3"):
     """The reference's own CPU run_case (oracle/_ref, threads-as-ranks on all
     host cores), timed by its own timer over iterations 2..N; a bounded
-    sample of `grid` (a few iterations). Checker/baseline only."""
+    sample of `grid` (a few iterations). Checker/baseline only: nothing here
+    loads libcavity_b200.so."""
     from oracle.refbind import Ref, Oracle, default_config, ref_available
     cores = os.cpu_count() or 1
     if ref_available():
-        np_ = min(cores, 512)
-        while np_ > 1:
-            try:
-                from paper_2006_02602_b200 import capi
-                dims = capi.choose_dims(np_, mode)
-                capi.partition(grid, dims)
-                break
-            except Exception:
-                np_ -= 1
+        np_, dims = ref_decomposition(grid, mode, min(cores, 512))
         cfg = default_config(grid=grid, steps=3, np=np_, mode=mode, strategy=strategy)
         r = Ref.run_case(cfg, collect_fields=False)
         per = max(r["wall_time_s"] / max(1, r["steps_timed"]), 1e-6)
@@ -171,8 +194,10 @@ def cpu_reference(grid, seconds_budget, mode="3d", strategy="v3"):
         return {"value": value, "unit": UNIT, "cores": np_, "kind": "reference",
                 "sample": f"{grid[0]}x{grid[1]}x{grid[2]}, {steps} iterations ({r['steps_timed']} timed, "
                           f"iteration 1 excluded as in src/runner.cpp:186), np={np_} threads "
-                          f"(3d dims {r['dims']}), reference AVX2 backend, {r['wall_time_s']:.2f} s",
-                "ms_per_step": 1e3 * r["wall_time_s"] / r["steps_timed"]}
+                          f"({mode} dims {tuple(r['dims'])}), reference AVX2 backend, {r['wall_time_s']:.2f} s",
+                "ms_per_step": 1e3 * r["wall_time_s"] / r["steps_timed"],
+                "decomposition": {"np": np_, "dims": list(r["dims"]), "iterations": steps,
+                                  "timed_iterations": r["steps_timed"]}}
     # plain-C oracle port, one core, on a smaller bounded sample
     g = (min(grid[0], 96),) * 3
     cfg = default_config(grid=g, steps=6)
@@ -180,7 +205,8 @@ def cpu_reference(grid, seconds_budget, mode="3d", strategy="v3"):
     cells = g[0] * g[1] * g[2]
     return {"value": cells * r["steps_timed"] / r["wall_time_s"] / 1e6, "unit": UNIT, "cores": 1,
             "kind": "port", "sample": f"{g} x 6 iterations, scalar C oracle",
-            "ms_per_step": 1e3 * r["wall_time_s"] / r["steps_timed"]}
+            "ms_per_step": 1e3 * r["wall_time_s"] / r["steps_timed"],
+            "decomposition": {"np": 1, "dims": [1, 1, 1], "iterations": 6, "timed_iterations": 5}}
 
 
 def dist_setup(n):
@@ -194,40 +220,59 @@ def dist_setup(n):
     return dist, dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def config_dict(args, grid, dims, n, build):
+def config_dict(args, grid, n):
+    """The workload, identical in both arms (implementation details such as the
+    rank layout and the build go in top-level keys)."""
     return {"workload": ("C1: 3D buoyancy-driven cavity 256^3 on 1 B200, FP64" if n == 1 and
                          tuple(grid) == (256, 256, 256) else
                          f"{args.scaling} scaling, {grid[0]}x{grid[1]}x{grid[2]} global on {n} B200"),
-            "grid": list(grid), "dims": list(dims), "mode": args.mode, "strategy": args.strategy,
+            "grid": list(grid), "mode": args.mode, "strategy": args.strategy,
             "overlap": bool(args.overlap and n > 1), "physics": "Ra=1e5, Pr=0.71, cfl=0.4, rescale on",
             "norm_history": "off (run_bench semantics, src/bench.cpp:44)",
-            "l2": "inputs larger than L2 (two 5-field states >> 126 MB)",
-            "build": build}
+            "l2": "inputs larger than L2 (two 5-field states >> 126 MB)"}
 
 
 def run_reference_arm(args):
-    dist, rank, world, _ = dist_setup(args.gpus)
-    n = args.gpus
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
+    """The unmodified reference CPU solver (oracle/_ref) on the host cores, on
+    this arm's workload. Under a multi-rank launch only rank 0 works."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    grid = grid_of(args, n)
-    from paper_2006_02602_b200 import capi
-    dims = capi.choose_dims(n, args.mode)
+    n = args.gpus
+    grid = grid_of(args, n, reference=True)
     cb = cpu_reference(grid, seconds_budget=min(120.0, max(10.0, args.cpu_seconds * 2)),
                        mode=args.mode, strategy=args.strategy)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (quiescent initial condition)",
-            "config": config_dict(args, grid, dims, n, "reference C++ (oracle/_ref, unmodified sources)"),
+            "data": "synthetic (quiescent initial condition, deterministic physics)",
+            "config": config_dict(args, grid, n),
+            "build": "reference C++ (oracle/_ref, unmodified sources, -O2 -ffp-contract=off, AVX2 backend)",
+            "decomposition": cb["decomposition"],
             "impl": "reference",
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+
+
+def spawn_ranks(n, cmd=None):
+    """`bench.py --gpus N` outside torchrun: one worker process per rank
+    (RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* set as torchrun would), device =
+    local rank modulo the visible GPUs; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK=str(r), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen(cmd or [sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
 
 
 def run_ours(args):
@@ -283,13 +328,20 @@ def run_ours(args):
 
     value = cells * args.steps / (total_ms * 1e-3) / 1e6
     peak, peak_src = measured_hbm()
-    achieved = BYTES_PER_CELL * cells_local / (step_ms * 1e-3) / 1e9
+    # the timed step launch covers the internal box when overlapping (the
+    # shells are a separate kernel), else the block's whole interior
+    blk_n = tuple(blk.n)
+    kcells = cells_local
+    if n > 1 and args.overlap:
+        lo, hi = capi.overlap_regions(blk_n, capi.neighbors(dims, rank))[0]
+        kcells = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
+    achieved = BYTES_PER_CELL * kcells / (step_ms * 1e-3) / 1e9
     traffic = step_traffic()
     tkey = f"{grid[0]}x{grid[1]}x{grid[2]}"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": (traffic or {}).get(tkey),
             "kernel": "k_step_tma (TMA-fed fused BC+residual+update+dt+rescale)",
-            "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells_local,
+            "algorithmic_bytes_per_launch": BYTES_PER_CELL * kcells,
             "kernel_ms": step_ms, "peak_source": peak_src,
             "step_share": step_ms * args.steps / total_ms if total_ms > 0 else None}
 
@@ -337,10 +389,15 @@ def run_ours(args):
         pub = PUBLISHED.get((args.scaling, n, tuple(grid)))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": args.scaling, "vs_baseline": (value / pub) if pub else None, "dtype": "f64",
+                "scaling": args.scaling, "vs_baseline": (value / pub) if pub else None,
+                "vs_baseline_source": (f"BASELINE.md published P100 OpenACC figure, {pub:.0f} MCUPS aggregate "
+                                       "(PAPER.md:358/:367-398); not the CPU reference") if pub else None,
+                "vs_cpu_baseline": (value / cpu["value"]) if cpu else None, "dtype": "f64",
                 "data": "synthetic (quiescent initial condition, deterministic physics)",
-                "config": config_dict(args, grid, dims, n,
-                                      capi.version(args.fmad)),
+                "config": config_dict(args, grid, n),
+                "build": capi.version(args.fmad),
+                "decomposition": {"np": n, "dims": list(dims), "block": list(blk_n),
+                                  "step_kernel_box_cells": kcells},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches,
                 "hbm_frac_of_step": BYTES_PER_CELL * cells / (total_ms * 1e-3 / args.steps) / 1e9 / n / peak,
@@ -358,6 +415,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     else:
         run_ours(args)
 
