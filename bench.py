@@ -315,32 +315,30 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(device) as clk:
-        total_ms, step_ms = blk.bench(args.steps)
+        total_ms, step_ms, wait_ms = blk.bench(args.steps)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    t = torch.tensor([total_ms, step_ms], dtype=torch.float64)
+    t = torch.tensor([total_ms, step_ms, wait_ms], dtype=torch.float64)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, step_ms_max = float(t[0]), float(t[1])
+    total_ms, step_ms_max, wait_ms_max = float(t[0]), float(t[1]), float(t[2])
     launches = blk.launches_per_iteration() * args.steps
     blk.close()
 
     value = cells * args.steps / (total_ms * 1e-3) / 1e6
     peak, peak_src = measured_hbm()
-    # the timed step launch covers the internal box when overlapping (the
-    # shells are a separate kernel), else the block's whole interior
+    # the step kernel covers the block's whole interior per iteration (two
+    # launches, internal then shell items, when overlapping; step_ms is their sum)
     blk_n = tuple(blk.n)
     kcells = cells_local
-    if n > 1 and args.overlap:
-        lo, hi = capi.overlap_regions(blk_n, capi.neighbors(dims, rank))[0]
-        kcells = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
     achieved = BYTES_PER_CELL * kcells / (step_ms * 1e-3) / 1e9
     traffic = step_traffic()
     tkey = f"{grid[0]}x{grid[1]}x{grid[2]}"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": (traffic or {}).get(tkey),
             "kernel": "k_step_tma (TMA-fed fused BC+residual+update+dt+rescale)",
+            "kernel_launches_per_iteration": 2 if (n > 1 and args.overlap) else 1,
             "algorithmic_bytes_per_launch": BYTES_PER_CELL * kcells,
             "kernel_ms": step_ms, "peak_source": peak_src,
             "step_share": step_ms * args.steps / total_ms if total_ms > 0 else None}
@@ -401,10 +399,11 @@ def run_ours(args):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches,
                 "hbm_frac_of_step": BYTES_PER_CELL * cells / (total_ms * 1e-3 / args.steps) / 1e9 / n / peak,
-                # share of the iteration outside the fused step kernel (halo pack/unpack, flag
-                # waits, overlap shells, scalar sync, launch gaps): the exposed-communication
-                # fraction at N > 1 (at N = 1 only launch gaps remain)
-                "exposed_comm_frac": (1.0 - roof["step_share"]) if roof["step_share"] is not None else None}
+                # time per iteration the compute stream waited for peers (their scalars, then
+                # the halo join after the internal items), device events, max over ranks,
+                # as a share of the iteration
+                "exposed_comm_frac": (wait_ms_max / (total_ms / args.steps)) if total_ms > 0 else None,
+                "exposed_comm_ms_per_step": wait_ms_max}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

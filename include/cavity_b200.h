@@ -38,6 +38,11 @@
 extern "C" {
 #endif
 
+/* Words per check iteration in cav_run_io.norm_digits: 5 x 70 carry-save
+ * digit words (the exact L2 sums), then the 5 L-inf maxima
+ * as bit patterns of max |R_v| (p,u,v,w,T), then padding. */
+#define CAV_NORM_WORDS 360
+
 /* ---- status codes (mirror the reference's exception taxonomy) ---------- */
 enum {
   CAV_OK = 0,
@@ -181,13 +186,15 @@ typedef struct {
   double conv_tol;
   int rescale;
   int check_every;
-  uint64_t seed;
+  uint64_t seed;        /* != 0: randomized rank timing (the InprocBus shuffle,
+                           src/inproc.cpp:92-114): rank threads start in a seeded
+                           order and each enqueues its iterations with seeded
+                           random pauses; results must not change */
   double timeout_ms;
   int monitor_every;
   double verify_tol;
   /* B200 extensions (no reference analogue) */
   int devices[8];       /* device of rank r is devices[r % 8]; default all 0 */
-  int chunk;            /* iterations captured per CUDA graph (0 = auto) */
 } cav_run_config;
 
 /* RunConfig defaults (Ra = 1e5, v3, 32^3, converge). */
@@ -229,6 +236,7 @@ typedef struct {
   double* hist_l2;      /* 5 per sample */
   int ledger_capacity;
   cav_ledger* ledgers;
+  double* hist_linf;    /* 5 per sample (max |R_v| over the global interior), or NULL */
 } cav_case_result;
 
 /* run_case (src/runner.cpp:259-338): one host thread per rank, one block per
@@ -253,7 +261,8 @@ typedef struct {
   int rescale;
   int corrupt_exchange;     /* ExchangePlan.corrupt_first hook */
   int device;
-  double timeout_ms;        /* device-side wait limit for peers */
+  double timeout_ms;        /* limit on waiting for a peer (TransportTimeout) */
+  uint64_t jitter_seed;     /* != 0: seeded random host pauses between iterations (tests) */
 } cav_block_desc;
 
 int cav_block_create(const cav_block_desc* desc, cav_block** out);
@@ -273,14 +282,15 @@ int cav_block_download(cav_block* b, double* host5);
 /* Sets the quiescent initial condition (initialize_fields, src/solver.cpp:292). */
 int cav_block_initialize(cav_block* b);
 
-/* Per-run outputs of cav_block_run. norm_limbs: per check iteration, 5*70
- * u64 carry-save digits, this rank's partial. */
+/* Per-run outputs of cav_block_run. norm_digits: per check iteration,
+ * CAV_NORM_WORDS u64 words (5*70 carry-save digits of the exact L2 sums, see
+ * DESIGN.md "exact norms", then 5 L-inf bit patterns), this rank's partial. */
 typedef struct {
   long long first_it;       /* iteration number of the first step (1-based) */
   long long n_its;
   int check_every;
   int want_norms;
-  uint64_t* norm_digits;    /* n_checks * 5 * 70, or NULL */
+  uint64_t* norm_digits;    /* n_checks * CAV_NORM_WORDS, or NULL */
   long long* check_iters;   /* n_checks, or NULL */
   long long n_checks;       /* out */
   long long err_iteration;  /* out: 0 = no error */
@@ -310,10 +320,12 @@ int cav_block_debug(cav_block* b, uint64_t* out, int cap);
 /* Last dt used and the current centre pressure shift (diagnostics). */
 int cav_block_scalars(cav_block* b, double* dt_out, double* pc_out);
 
-/* Fused-step bench hook: time n_its iterations with CUDA events on the
- * block's stream, no host sync inside; returns per-launch average of the
- * dominant (fused step) kernel in *step_kernel_ms. */
-int cav_block_bench(cav_block* b, long long n_its, double* total_ms, double* step_kernel_ms);
+/* Bench hook: time n_its iterations with CUDA events on the block's compute
+ * stream. out[0] total ms; out[1] fused-step kernel ms per iteration (both
+ * launches when overlapping); out[2] ms per iteration the compute stream
+ * spent waiting for peers (scalars, then the halo join): the exposed
+ * communication. */
+int cav_block_bench(cav_block* b, long long n_its, double out[3]);
 
 #ifdef __cplusplus
 }

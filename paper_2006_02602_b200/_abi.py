@@ -48,6 +48,9 @@ class FieldPtrs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("p", "u", "v", "w", "t")]
 
 
+NORM_WORDS = 360  # CAV_NORM_WORDS: 5 x 70 digits, 5 L-inf bit patterns, padding
+
+
 class PlanEntry(C.Structure):
     _fields_ = [("face", C.c_int), ("neighbor", C.c_int), ("nvars", C.c_int),
                 ("var", C.c_int * 5), ("depth", C.c_int * 5), ("scalars", C.c_longlong),
@@ -61,7 +64,7 @@ class RunConfig(C.Structure):
                 ("cfl", C.c_double), ("max_steps", C.c_longlong), ("conv_tol", C.c_double),
                 ("rescale", C.c_int), ("check_every", C.c_int), ("seed", C.c_uint64),
                 ("timeout_ms", C.c_double), ("monitor_every", C.c_int),
-                ("verify_tol", C.c_double), ("devices", C.c_int * 8), ("chunk", C.c_int)]
+                ("verify_tol", C.c_double), ("devices", C.c_int * 8)]
 
 
 class CaseOptions(C.Structure):
@@ -87,7 +90,7 @@ class CaseResultC(C.Structure):
                 ("fields", C.POINTER(C.c_double)), ("hist_capacity", C.c_longlong),
                 ("hist_count", C.c_longlong), ("hist_iter", C.POINTER(C.c_longlong)),
                 ("hist_l2", C.POINTER(C.c_double)), ("ledger_capacity", C.c_int),
-                ("ledgers", C.POINTER(Ledger))]
+                ("ledgers", C.POINTER(Ledger)), ("hist_linf", C.POINTER(C.c_double))]
 
 
 class BlockDesc(C.Structure):
@@ -95,7 +98,7 @@ class BlockDesc(C.Structure):
                 ("gnz", C.c_int), ("dims", C.c_int * 3), ("strategy", C.c_int),
                 ("overlap", C.c_int), ("fluid", FluidParams), ("cfl", C.c_double),
                 ("rescale", C.c_int), ("corrupt_exchange", C.c_int), ("device", C.c_int),
-                ("timeout_ms", C.c_double)]
+                ("timeout_ms", C.c_double), ("jitter_seed", C.c_uint64)]
 
 
 class RunIO(C.Structure):

@@ -153,6 +153,7 @@ class CaseResult:
     history: np.ndarray
     ledgers: List[dict]
     fields: Optional[np.ndarray] = None  # (5, nz, ny, nx): p,u,v,w,T
+    history_linf: Optional[np.ndarray] = None  # (samples, 5): max |R_v| per check iteration
 
     def __getitem__(self, k):  # dict-style access, like the oracle results
         return getattr(self, k)
@@ -167,6 +168,7 @@ def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=
     cap = int(target // max(1, cfg.check_every) + 2)
     hist_iter = np.zeros(cap, dtype=np.int64)
     hist_l2 = np.zeros(5 * cap)
+    hist_linf = np.zeros(5 * cap)
     nl = max(1, cfg.np)
     led = (A.Ledger * nl)()
     out = A.CaseResultC()
@@ -174,6 +176,7 @@ def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=
     out.hist_capacity = cap
     out.hist_iter = hist_iter.ctypes.data_as(C.POINTER(C.c_longlong))
     out.hist_l2 = hist_l2.ctypes.data_as(C.POINTER(C.c_double))
+    out.hist_linf = hist_linf.ctypes.data_as(C.POINTER(C.c_double))
     out.ledger_capacity = nl
     out.ledgers = C.cast(led, C.POINTER(A.Ledger))
     opt = A.CaseOptions(int(collect_fields), int(collect_history), int(corrupt_exchange))
@@ -186,7 +189,8 @@ def run_case(cfg, collect_fields=False, collect_history=False, corrupt_exchange=
         wall_time_s=out.wall_time_s, ssspnt=out.ssspnt, bytes_sent=out.bytes_sent,
         history_iter=hist_iter[:h].copy(), history=hist_l2[:5 * h].reshape(h, 5).copy(),
         ledgers=[led[r].as_dict() for r in range(out.np)],
-        fields=fields.reshape(5, cfg.nz, cfg.ny, cfg.nx) if fields is not None else None)
+        fields=fields.reshape(5, cfg.nz, cfg.ny, cfg.nx) if fields is not None else None,
+        history_linf=hist_linf[:5 * h].reshape(h, 5).copy())
 
 
 @dataclass
@@ -381,7 +385,7 @@ class Block:
     the arenas are exchanged as CUDA IPC handles (see bench.py)."""
 
     def __init__(self, rank, np_, grid, dims, strategy="v3", overlap=False, fluid=None, cfl=0.4,
-                 rescale=True, corrupt_exchange=False, device=0, timeout_ms=20000.0):
+                 rescale=True, corrupt_exchange=False, device=0, timeout_ms=20000.0, jitter_seed=0):
         self.L = lib()
         d = A.BlockDesc()
         d.rank, d.np = rank, np_
@@ -396,6 +400,7 @@ class Block:
         d.corrupt_exchange = int(corrupt_exchange)
         d.device = device
         d.timeout_ms = timeout_ms
+        d.jitter_seed = jitter_seed
         self.desc = d
         self.h = C.c_void_p()
         check(self.L.cav_block_create(C.byref(d), C.byref(self.h)))
@@ -450,12 +455,14 @@ class Block:
         return out
 
     def run(self, n_its, check_every=10, want_norms=False):
-        """March n_its iterations; returns (seconds, [(iteration, digits[5,70])])."""
+        """March n_its iterations; returns (seconds, [(iteration, digits[5,70], linf_bits[5])])
+        with this rank's exact-norm partials per check iteration."""
         cadence = max(1, check_every)
         first = self.next_it
         nchk = sum(1 for it in range(first, first + n_its)
                    if want_norms and (it == 1 or it % cadence == 0))
-        dig = np.zeros(max(1, nchk) * 350, dtype=np.uint64)
+        W = A.NORM_WORDS
+        dig = np.zeros(max(1, nchk) * W, dtype=np.uint64)
         iters = np.zeros(max(1, nchk), dtype=np.int64)
         io = A.RunIO()
         io.first_it, io.n_its, io.check_every, io.want_norms = first, n_its, cadence, int(want_norms)
@@ -466,15 +473,16 @@ class Block:
         self.ledger = io.ledger
         check(st)
         self.next_it += n_its
-        return io.seconds, [(int(iters[c]), dig[c * 350:(c + 1) * 350].reshape(5, 70))
-                            for c in range(io.n_checks)]
+        return io.seconds, [(int(iters[c]), dig[c * W:c * W + 350].reshape(5, 70),
+                             dig[c * W + 350:c * W + 355].copy()) for c in range(io.n_checks)]
 
     def bench(self, n_its):
-        total = C.c_double()
-        step = C.c_double()
-        check(self.L.cav_block_bench(self.h, n_its, C.byref(total), C.byref(step)))
+        """Times n_its iterations: (total ms, step-kernel ms per iteration,
+        ms per iteration spent waiting on peers)."""
+        out = (C.c_double * 3)()
+        check(self.L.cav_block_bench(self.h, n_its, out))
         self.next_it += n_its
-        return total.value, step.value
+        return out[0], out[1], out[2]
 
     def launches_per_iteration(self):
         return self.L.cav_block_launches_per_iteration(self.h, 0)

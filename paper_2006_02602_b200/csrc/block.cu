@@ -30,6 +30,8 @@
 #include <cudaTypedefs.h>
 
 #include <chrono>
+#include <cstddef>
+#include <thread>
 
 #include <cstdlib>
 
@@ -42,357 +44,6 @@
 namespace cav {
 
 // ---------------------------------------------------------------------------
-// Fused step, tiled: 32 x TY threads own (i,j) columns of one tile and stream
-// k. Pressure k-2..k+2 and u,v,w,T k-1..k+1 of the own column sit in
-// registers; the in-plane neighbours come from a double-buffered shared-memory
-// plane with a cross-shaped halo (2 for p, 1 for the rest; corners are never
-// read). Next-plane loads are issued before the current plane is computed.
-struct StepArgs {
-  const double* in;
-  double* out;
-  Geo g;
-  cav_stencil_params sp;
-  BetaFast bf;  // beta shortcuts (host::beta_fast)
-  cav_box box;
-  int kchunk;
-  const IterScalars* sc;
-  Acc* acc;
-  unsigned long long* digits;  // 5*70 for check iterations, else null
-  int cx, cy, cz;              // centre node storage coords on the owner, else -1
-  long long n;
-  int rank;
-};
-
-template <int NT, bool NORMS>
-__device__ __forceinline__ void step_epilogue(const StepArgs& a, double m0, double m1, double m2, unsigned bad,
-                                              unsigned nbad, unsigned long long* sdig) {
-  block_reduce_max3_or<NT>(m0, m1, m2, bad);
-  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
-  if (tid == 0) acc_publish(a.acc, m0, m1, m2, bad, a.n + 1, a.rank);
-  if (NORMS) {
-    nbad = __syncthreads_or(nbad);
-    if (tid == 0 && nbad) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
-    for (int x = tid; x < 5 * kDigits; x += NT)
-      if (sdig[x]) atomicAdd(&a.digits[x], sdig[x]);
-  }
-}
-
-template <int TY, bool NORMS>
-__global__ void __launch_bounds__(32 * TY, 2) k_step_tiled(const StepArgs a) {
-  constexpr int TX = 32, NT = TX * TY;
-  constexpr int PW = TX + 4, PH = TY + 4, QW = TX + 2, QH = TY + 2;
-  constexpr int PLANE_P = PH * PW, PLANE_Q = QH * QW;
-  constexpr int BUF = PLANE_P + 4 * PLANE_Q;
-  constexpr int NH = 12 * TX + 12 * TY;  // halo elements per plane (p: 4TX+4TY, q: 4*(2TX+2TY))
-  constexpr int NS = (NH + NT - 1) / NT;
-  __shared__ __align__(16) double sm[2 * BUF];
-  __shared__ unsigned long long sdig[NORMS ? 5 * kDigits : 1];
-
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const Geo g = a.g;
-  const int ti0 = a.box.lo[0] + blockIdx.x * TX, tj0 = a.box.lo[1] + blockIdx.y * TY;
-  const int i = ti0 + tx, j = tj0 + ty;
-  const int kb = a.box.lo[2] + blockIdx.z * a.kchunk;
-  const int ke = min(kb + a.kchunk, a.box.hi[2]);
-  const bool active = i < a.box.hi[0] && j < a.box.hi[1];
-  const bool inst = i < g.nx + 4 && j < g.ny + 4;
-  const bool ij_int = i >= 2 && i < g.nx + 2 && j >= 2 && j < g.ny + 2;
-  const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
-  const long long fs = g.fstride;
-  const double pc = a.sc->pc, dt = a.sc->dt;
-  const double* __restrict__ in = a.in;
-  double* __restrict__ out = a.out;
-  const long long col = g.idx(i, j, 0);
-  const int kzl = 2, kzh = g.nz + 2, kst = g.nz + 4;
-
-  if (NORMS) {
-    for (int x = tid; x < 5 * kDigits; x += NT) sdig[x] = 0;
-  }
-
-  // halo slots: (source column pointer, smem offset, shiftable)
-  const double* hsrc[NS];
-  int hdst[NS];
-  bool hsh[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    const int h = tid + s * NT;
-    hsrc[s] = nullptr;
-    hdst[s] = 0;
-    hsh[s] = false;
-    if (h < NH) {
-      int f, ii, jj, so;
-      if (h < 4 * TX + 4 * TY) {  // pressure, 2-wide cross halo
-        f = 0;
-        if (h < 2 * TX) {
-          const int r = h / TX, c = h % TX;
-          ii = ti0 + c;
-          jj = tj0 - 2 + r;
-          so = r * PW + 2 + c;
-        } else if (h < 4 * TX) {
-          const int e = h - 2 * TX, r = e / TX, c = e % TX;
-          ii = ti0 + c;
-          jj = tj0 + TY + r;
-          so = (TY + 2 + r) * PW + 2 + c;
-        } else if (h < 4 * TX + 2 * TY) {
-          const int e = h - 4 * TX, c = e / TY, r = e % TY;
-          ii = ti0 - 2 + c;
-          jj = tj0 + r;
-          so = (r + 2) * PW + c;
-        } else {
-          const int e = h - 4 * TX - 2 * TY, c = e / TY, r = e % TY;
-          ii = ti0 + TX + c;
-          jj = tj0 + r;
-          so = (r + 2) * PW + TX + 2 + c;
-        }
-      } else {  // u, v, w, T, 1-wide cross halo
-        const int e0 = h - (4 * TX + 4 * TY);
-        f = 1 + e0 / (2 * TX + 2 * TY);
-        const int e = e0 % (2 * TX + 2 * TY);
-        int r, c;
-        if (e < TX) {
-          ii = ti0 + e;
-          jj = tj0 - 1;
-          r = 0;
-          c = 1 + e;
-        } else if (e < 2 * TX) {
-          ii = ti0 + e - TX;
-          jj = tj0 + TY;
-          r = TY + 1;
-          c = 1 + e - TX;
-        } else if (e < 2 * TX + TY) {
-          ii = ti0 - 1;
-          jj = tj0 + e - 2 * TX;
-          r = 1 + e - 2 * TX;
-          c = 0;
-        } else {
-          ii = ti0 + TX;
-          jj = tj0 + e - 2 * TX - TY;
-          r = 1 + e - 2 * TX - TY;
-          c = TX + 1;
-        }
-        so = PLANE_P + (f - 1) * PLANE_Q + r * QW + c;
-      }
-      hdst[s] = so;
-      if (ii >= 0 && ii < g.nx + 4 && jj >= 0 && jj < g.ny + 4) {
-        hsrc[s] = in + f * fs + g.idx(ii, jj, 0);
-        hsh[s] = f == 0 && ii >= 2 && ii < g.nx + 2 && jj >= 2 && jj < g.ny + 2;
-      }
-    }
-  }
-
-  auto ldc = [&](int f, int k) -> double {
-    return (inst && k >= 0 && k < kst) ? in[f * fs + col + k * plane] : 0.0;
-  };
-  auto shift_at = [&](bool ijok, int k) -> double { return (ijok && k >= kzl && k < kzh) ? pc : 0.0; };
-
-  double pm2 = ldc(0, kb - 2) - shift_at(ij_int, kb - 2);
-  double pm1 = ldc(0, kb - 1) - shift_at(ij_int, kb - 1);
-  double p0 = ldc(0, kb) - shift_at(ij_int, kb);
-  double pp1 = ldc(0, kb + 1) - shift_at(ij_int, kb + 1);
-  double pp2 = ldc(0, kb + 2) - shift_at(ij_int, kb + 2);
-  double um1 = ldc(1, kb - 1), u0 = ldc(1, kb), up1 = ldc(1, kb + 1);
-  double vm1 = ldc(2, kb - 1), v0 = ldc(2, kb), vp1 = ldc(2, kb + 1);
-  double wm1 = ldc(3, kb - 1), w0 = ldc(3, kb), wp1 = ldc(3, kb + 1);
-  double tm1 = ldc(4, kb - 1), t0 = ldc(4, kb), tp1 = ldc(4, kb + 1);
-  double hcur[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) hcur[s] = (hsrc[s] && kb < ke) ? hsrc[s][kb * plane] : 0.0;
-
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-  unsigned bad = 0, nbad = 0;
-  const double u_ref = a.sp.u_ref;
-
-  for (int k = kb; k < ke; ++k) {
-    const bool more = k + 1 < ke;
-    // issue next-plane loads first; they land while this plane computes
-    const double np3 = more ? ldc(0, k + 3) : 0.0;
-    const double nu2 = more ? ldc(1, k + 2) : 0.0;
-    const double nv2 = more ? ldc(2, k + 2) : 0.0;
-    const double nw2 = more ? ldc(3, k + 2) : 0.0;
-    const double nt2 = more ? ldc(4, k + 2) : 0.0;
-    double hnext[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) hnext[s] = (more && hsrc[s]) ? hsrc[s][(k + 1) * plane] : 0.0;
-
-    double* B = sm + (k & 1) * BUF;
-    B[(ty + 2) * PW + tx + 2] = p0;
-    double* BQ = B + PLANE_P + (ty + 1) * QW + tx + 1;
-    BQ[0] = u0;
-    BQ[PLANE_Q] = v0;
-    BQ[2 * PLANE_Q] = w0;
-    BQ[3 * PLANE_Q] = t0;
-    const bool kint = k >= kzl && k < kzh;
-#pragma unroll
-    for (int s = 0; s < NS; ++s)
-      if (tid + s * NT < NH) B[hdst[s]] = hcur[s] - ((hsh[s] && kint) ? pc : 0.0);
-    __syncthreads();
-
-    if (active) {
-      const double* BP = B + (ty + 2) * PW + tx + 2;
-      Star st;
-      st.p = p0;
-      st.pxm = BP[-1];
-      st.pxp = BP[1];
-      st.pxm2 = BP[-2];
-      st.pxp2 = BP[2];
-      st.pym = BP[-PW];
-      st.pyp = BP[PW];
-      st.pym2 = BP[-2 * PW];
-      st.pyp2 = BP[2 * PW];
-      st.pzm = pm1;
-      st.pzp = pp1;
-      st.pzm2 = pm2;
-      st.pzp2 = pp2;
-      const double* BU = BQ;
-      st.u = u0;
-      st.uxm = BU[-1];
-      st.uxp = BU[1];
-      st.uym = BU[-QW];
-      st.uyp = BU[QW];
-      st.uzm = um1;
-      st.uzp = up1;
-      const double* BV = BQ + PLANE_Q;
-      st.v = v0;
-      st.vxm = BV[-1];
-      st.vxp = BV[1];
-      st.vym = BV[-QW];
-      st.vyp = BV[QW];
-      st.vzm = vm1;
-      st.vzp = vp1;
-      const double* BW = BQ + 2 * PLANE_Q;
-      st.w = w0;
-      st.wxm = BW[-1];
-      st.wxp = BW[1];
-      st.wym = BW[-QW];
-      st.wyp = BW[QW];
-      st.wzm = wm1;
-      st.wzp = wp1;
-      const double* BT = BQ + 3 * PLANE_Q;
-      st.t = t0;
-      st.txm = BT[-1];
-      st.txp = BT[1];
-      st.tym = BT[-QW];
-      st.typ = BT[QW];
-      st.tzm = tm1;
-      st.tzp = tp1;
-      const Res r = residual_of(st, a.sp, a.bf);
-      // euler_step: q = q + dt*r (src/solver.cpp:239-246)
-      const double qp = p0 + dt * r.p, qu = u0 + dt * r.u, qv = v0 + dt * r.v, qw = w0 + dt * r.w,
-                   qt = t0 + dt * r.t;
-      const long long c = col + k * plane;
-      out[c] = qp;
-      out[fs + c] = qu;
-      out[2 * fs + c] = qv;
-      out[3 * fs + c] = qw;
-      out[4 * fs + c] = qt;
-      const Denoms d = cfl_denoms(qu, qv, qw, u_ref, a.bf);
-      m0 = dmax_d(m0, d.du);
-      m1 = dmax_d(m1, d.dv);
-      m2 = dmax_d(m2, d.dw);
-      bad |= nonfinite(qp) | (nonfinite(qu) << 1) | (nonfinite(qv) << 2) | (nonfinite(qw) << 3) |
-             (nonfinite(qt) << 4);
-      if (i == a.cx && j == a.cy && k == a.cz) a.acc->pc_local = qp;
-      if (NORMS) {
-        const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
-#pragma unroll
-        for (int v = 0; v < 5; ++v) {
-          if (nonfinite(rr[v])) nbad = 1;
-          else add_term_digits(sdig + v * kDigits, rr[v]);
-        }
-      }
-    }
-
-    pm2 = pm1;
-    pm1 = p0;
-    p0 = pp1;
-    pp1 = pp2;
-    pp2 = np3 - shift_at(ij_int, k + 3);
-    um1 = u0;
-    u0 = up1;
-    up1 = nu2;
-    vm1 = v0;
-    v0 = vp1;
-    vp1 = nv2;
-    wm1 = w0;
-    w0 = wp1;
-    wp1 = nw2;
-    tm1 = t0;
-    t0 = tp1;
-    tp1 = nt2;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) hcur[s] = hnext[s];
-  }
-  __syncthreads();
-  step_epilogue<NT, NORMS>(a, m0, m1, m2, bad, nbad, sdig);
-}
-
-// Fused step, pointwise: one thread per cell of up to six boxes (the overlap
-// shells of src/overlap.cpp:13-28), neighbours straight from L1/L2.
-struct ShellArgs {
-  StepArgs s;
-  WallInfo walls;
-  int nbox;
-  cav_box box[6];
-  long long start[7];
-};
-
-constexpr int kShellThreads = 256;
-
-template <bool NORMS>
-__global__ void __launch_bounds__(kShellThreads) k_step_shells(const ShellArgs a) {
-  __shared__ unsigned long long sdig[NORMS ? 5 * kDigits : 1];
-  const StepArgs& s = a.s;
-  if (NORMS) {
-    for (int x = threadIdx.x; x < 5 * kDigits; x += kShellThreads) sdig[x] = 0;
-    __syncthreads();
-  }
-  const long long q = blockIdx.x * static_cast<long long>(kShellThreads) + threadIdx.x;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-  unsigned bad = 0, nbad = 0;
-  if (q < a.start[a.nbox]) {
-    int b = 0;
-    while (q >= a.start[b + 1]) ++b;
-    const cav_box& bx = a.box[b];
-    const long long e = q - a.start[b];
-    const int w = bx.hi[0] - bx.lo[0], h = bx.hi[1] - bx.lo[1];
-    const int i = bx.lo[0] + static_cast<int>(e % w);
-    const int j = bx.lo[1] + static_cast<int>((e / w) % h);
-    const int k = bx.lo[2] + static_cast<int>(e / (static_cast<long long>(w) * h));
-    const Geo& g = s.g;
-    const long long fs = g.fstride;
-    const double pc = s.sc->pc, dt = s.sc->dt;
-    Star st = load_star(s.in, s.in + fs, s.in + 2 * fs, s.in + 3 * fs, s.in + 4 * fs, g, i, j, k, pc);
-    if (near_wall(a.walls, g, i, j, k)) apply_wall_ghosts(st, a.walls, g, i, j, k);
-    const Res r = residual_of(st, s.sp, s.bf);
-    const double qp = st.p + dt * r.p, qu = st.u + dt * r.u, qv = st.v + dt * r.v, qw = st.w + dt * r.w,
-                 qt = st.t + dt * r.t;
-    const long long c = g.idx(i, j, k);
-    s.out[c] = qp;
-    s.out[fs + c] = qu;
-    s.out[2 * fs + c] = qv;
-    s.out[3 * fs + c] = qw;
-    s.out[4 * fs + c] = qt;
-    const Denoms d = cfl_denoms(qu, qv, qw, s.sp.u_ref, s.bf);
-    m0 = d.du;
-    m1 = d.dv;
-    m2 = d.dw;
-    bad = nonfinite(qp) | (nonfinite(qu) << 1) | (nonfinite(qv) << 2) | (nonfinite(qw) << 3) |
-          (nonfinite(qt) << 4);
-    if (i == s.cx && j == s.cy && k == s.cz) s.acc->pc_local = qp;
-    if (NORMS) {
-      const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        if (nonfinite(rr[v])) nbad = 1;
-        else add_term_digits(sdig + v * kDigits, rr[v]);
-      }
-    }
-  }
-  if (NORMS) __syncthreads();
-  step_epilogue<kShellThreads, NORMS>(s, m0, m1, m2, bad, nbad, sdig);
-}
-
-// ---------------------------------------------------------------------------
 // Halo exchange: one descriptor per plan entry (= one reference message).
 struct MsgDesc {
   int face;
@@ -401,61 +52,63 @@ struct MsgDesc {
   long long voff[6];  // payload offset of each variable's box (copy_box_to order)
   cav_box box[5];     // pack: face_interior_box; unpack: face_ghost_box
   long long scalars;
-  double* slab;               // pack: receiver's slab (parity 0); unpack: own slab
+  double* slab;               // pack: receiver's slab (parity 0); unpack: own slab (2 parities)
   unsigned long long* flag;   // pack: receiver's flag; unpack: own flag
   unsigned* counter;          // pack: CTA completion counter
   int peer;
 };
 
-// Progress stamps (diagnostics): stage -> last iteration that reached it.
-enum DbgStage { kDbgPackStart, kDbgPackFlag, kDbgWaitStart, kDbgWaitDone, kDbgUnpackDone, kDbgSyncPush,
-                kDbgSyncDone, kDbgStages };
-__device__ __forceinline__ void dbg_stamp(unsigned long long* dbg, int stage, long long n) {
-  if (dbg) atomicMax(dbg + stage, static_cast<unsigned long long>(n));
-}
+// Cross-rank values carry a generation in their high bits (one per run from
+// iteration 1, i.e. per upload/initialize), so a flag or stamp left by an
+// earlier run never satisfies a wait of the current one.
+constexpr int kGenShift = 40;
 
 struct XArgs {
-  unsigned long long* dbg;
   double* state;
   Geo g;
   const MsgDesc* msg;
-  long long n;
-  const IterScalars* sc;
+  long long n;              // iteration (slab parity)
+  unsigned long long val;   // flag value of this iteration (generation | n)
   int corrupt;
-  unsigned long long timeout_ns;
-  unsigned long long* timeout_flag;
-  int rank;
+  const int* abort;
 };
 
 constexpr int kXThreads = 256, kXItems = 4;
 
-__device__ __forceinline__ void msg_locate(const MsgDesc& m, long long q, int& v, int& i, int& j, int& k) {
+// payload element q of entry m -> (variable, storage cell); box volumes are
+// far below 2^31, so 32-bit index arithmetic suffices
+__device__ __forceinline__ void msg_locate(const MsgDesc& m, int q, int& v, int& i, int& j, int& k) {
   int s = 0;
   while (s + 1 < m.nvars && q >= m.voff[s + 1]) ++s;
   const cav_box& b = m.box[s];
-  const long long e = q - m.voff[s];
+  const int e = q - static_cast<int>(m.voff[s]);
   const int w = b.hi[0] - b.lo[0], h = b.hi[1] - b.lo[1];
-  i = b.lo[0] + static_cast<int>(e % w);
-  j = b.lo[1] + static_cast<int>((e / w) % h);
-  k = b.lo[2] + static_cast<int>(e / (static_cast<long long>(w) * h));
+  const int row = e / w;
+  i = b.lo[0] + (e - row * w);
+  const int k0 = row / h;
+  j = b.lo[1] + (row - k0 * h);
+  k = b.lo[2] + k0;
   v = m.var[s];
 }
 
+// exchange_begin (src/exchange.cpp:115-145): every plan entry's payload, in
+// copy_box_to order (src/slab.cpp:33-52), stored straight into the
+// neighbour's receive slab over NVLink / peer memory; the CTA that completes
+// an entry last releases the neighbour's flag (system scope).
 __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) dbg_stamp(a.dbg, kDbgPackStart, a.n);
+  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
   const MsgDesc& m = a.msg[blockIdx.y];
-  const double pc = a.sc->pc;
   double* dst = m.slab + (a.n & 1) * m.scalars;
-  const long long base = static_cast<long long>(blockIdx.x) * kXThreads * kXItems;
+  const int base = static_cast<int>(blockIdx.x) * kXThreads * kXItems;
+  if (base < m.scalars) {
 #pragma unroll
-  for (int it = 0; it < kXItems; ++it) {
-    const long long q = base + it * kXThreads + threadIdx.x;
-    if (q < m.scalars) {
-      int v, i, j, k;
-      msg_locate(m, q, v, i, j, k);
-      double x = a.state[v * a.g.fstride + a.g.idx(i, j, k)];
-      if (v == 0) x = x - pc;  // sender's interior is the rescaled field
-      dst[q] = x;              // remote store into the neighbour's slab
+    for (int it = 0; it < kXItems; ++it) {
+      const int q = base + it * kXThreads + static_cast<int>(threadIdx.x);
+      if (q < m.scalars) {
+        int v, i, j, k;
+        msg_locate(m, q, v, i, j, k);
+        dst[q] = a.state[v * a.g.fstride + a.g.idx(i, j, k)];  // remote store into the neighbour's slab
+      }
     }
   }
   __threadfence_system();
@@ -465,141 +118,183 @@ __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
     if (done == gridDim.x - 1) {
       *m.counter = 0;
       __threadfence_system();
-      st_release_sys(m.flag, static_cast<unsigned long long>(a.n));
-      dbg_stamp(a.dbg, kDbgPackFlag, a.n);
+      st_release_sys(m.flag, a.val);
     }
   }
 }
 
-// Waits for every receive flag of iteration n (acquire, system scope). One
-// small CTA, so a peer's pack can always find an SM even when several ranks
-// share one GPU (the in-process test topology).
-__global__ void __launch_bounds__(32) k_wait_flags(const XArgs a, int nmsg) {
-  if (*reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull) return;  // already failed
-  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgWaitStart, a.n);
-  for (int m = threadIdx.x; m < nmsg; m += 32) {
-    const unsigned long long t0 = globaltimer_ns();
-    while (ld_acquire_sys(a.msg[m].flag) < static_cast<unsigned long long>(a.n)) {
-      if (globaltimer_ns() - t0 > a.timeout_ns) {
-        atomicMin(a.timeout_flag, err_code(a.n, a.rank, 8 + a.msg[m].face));
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  __threadfence();
-  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgWaitDone, a.n);
-}
-
+// exchange_finish (src/exchange.cpp:147-176): the stream has waited for the
+// flags (cuStreamWaitValue64, no resident spinning); the acquire below orders
+// the slab reads after the peer's release, then copy_box_from
+// (src/slab.cpp:54-71) into the join ghosts.
 __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
+  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
   const MsgDesc& m = a.msg[blockIdx.y];
-  const long long base = static_cast<long long>(blockIdx.x) * kXThreads * kXItems;
+  const int base = static_cast<int>(blockIdx.x) * kXThreads * kXItems;
   if (base >= m.scalars) return;
+  if (ld_acquire_sys(m.flag) < a.val) return;  // only after an abort released the wait
   const double* src = m.slab + (a.n & 1) * m.scalars;
 #pragma unroll
   for (int it = 0; it < kXItems; ++it) {
-    const long long q = base + it * kXThreads + threadIdx.x;
+    const int q = base + it * kXThreads + static_cast<int>(threadIdx.x);
     if (q < m.scalars) {
       int v, i, j, k;
       msg_locate(m, q, v, i, j, k);
       double x = __ldcg(src + q);
-      if (a.corrupt && blockIdx.y == 0 && q == 0) x += 1e-3;  // exchange_finish's hook
+      if (a.corrupt && blockIdx.y == 0 && q == 0) x += 1e-3;  // exchange_finish's corrupt_first hook
       a.state[v * a.g.fstride + a.g.idx(i, j, k)] = x;
     }
   }
-  if (threadIdx.x == 0) dbg_stamp(a.dbg, kDbgUnpackDone, a.n);
 }
 
 // ---------------------------------------------------------------------------
-// Scalar exchange: every rank pushes (CFL maxima, centre pressure, error code)
-// into slot[rank][n&1] of every rank's arena, then folds all np slots.
+// Scalars between ranks (reduce_fixed_order(Min) of dt and the centre
+// pressure broadcast, src/transport.cpp:23-60, src/exchange.cpp:183-193),
+// folded so that one exchange per iteration suffices and every block can
+// store its rescaled pressure eagerly:
+//   k_push (after step n): this rank's CFL maxima and error code, plus the
+//     values of S_n it owns among the centre cell's stencil (the 13-point p
+//     star and the u, v, w values R_p reads), into slot[rank][n&1] of every
+//     rank's arena, then a release of the slot's stamp;
+//   k_fold (before step n+1, after the stream waited for every stamp):
+//     dt_{n+1} from the global maxima (the exact max rewrite of compute_dt)
+//     and pcs_{n+1} = p'(centre) of step n+1 from the gathered star — the
+//     residual and update of that one cell with the step's own arithmetic —
+//     so step n+1 stores fl(p' - pcs_{n+1}) exactly as rescale_pressure
+//     (src/solver.cpp:248-257) would leave it.
+// Star order: p, p-x, p+x, p-2x, p+2x, p-y, p+y, p-2y, p+2y, p-z, p+z, p-2z,
+// p+2z, u, u-x, u+x, v, v-y, v+y, w, w-z, w+z.
+constexpr int kStar = 22;
 struct Slot {
   unsigned long long d[3];
-  double pc;
   unsigned long long err;
   unsigned long long stamp;
-  unsigned long long pad[2];
+  unsigned long long pad[3];
+  double star[24];
 };
-static_assert(sizeof(Slot) == 64, "slot size");
+static_assert(sizeof(Slot) == 256, "slot size");
 
-struct SyncArgs {
-  unsigned long long* dbg;
-  Acc* acc_cur;
-  Acc* acc_next;
-  IterScalars* sc_next;
-  Slot* my_slots;              // this rank's arena slots [np][2]
-  Slot* const* peer_slots;     // device array: rank r's slot base
-  int np, rank, owner;
-  long long n;
-  double dx, dy, dz, cfl;
-  cav_fluid_params fl;
-  int rescale;
-  unsigned long long* err_sticky;
-  unsigned long long timeout_ns;
-  unsigned long long* timeout_flag;
+struct StarCells {       // this rank's share of the centre star
+  int n;
+  int slot[kStar];
+  int var[kStar];
+  long long idx[kStar];  // storage index within the field
 };
 
-constexpr int kSyncThreads = 128;
+struct PushArgs {
+  const Acc* acc;
+  const double* state;   // S_n (the step's output)
+  long long fstride;
+  StarCells mine;
+  Slot* const* peer_slots;
+  int np, rank, par;
+  unsigned long long stamp;
+  const int* abort;
+};
 
-__global__ void __launch_bounds__(kSyncThreads) k_scalar_sync(const SyncArgs a) {
-  __shared__ unsigned long long sd[3][kSyncThreads];
-  __shared__ unsigned long long se[kSyncThreads];
-  __shared__ double spc;
-  const int tid = threadIdx.x;
-  const int par = static_cast<int>(a.n & 1);
-  const Acc mine = *a.acc_cur;
-  if (tid == 0) spc = 0.0;
-  for (int r = tid; r < a.np; r += kSyncThreads) {
-    Slot* s = a.peer_slots[r] + (a.rank * 2 + par);
+__global__ void __launch_bounds__(32) k_push(const PushArgs a) {
+  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
+  __shared__ double st[kStar];
+  const int t = threadIdx.x;
+  if (t < kStar) st[t] = 0.0;
+  __syncwarp();
+  if (t < a.mine.n) st[a.mine.slot[t]] = a.state[a.mine.var[t] * a.fstride + a.mine.idx[t]];
+  __syncwarp();
+  const Acc mine = *a.acc;
+  for (int r = t; r < a.np; r += 32) {
+    Slot* s = a.peer_slots[r] + (a.rank * 2 + a.par);
     s->d[0] = mine.dmax[0];
     s->d[1] = mine.dmax[1];
     s->d[2] = mine.dmax[2];
-    s->pc = mine.pc_local;
     s->err = mine.err;
+    for (int q = 0; q < kStar; ++q) s->star[q] = st[q];
     __threadfence_system();
-    st_release_sys(&s->stamp, static_cast<unsigned long long>(a.n) + 1);
+    st_release_sys(&s->stamp, a.stamp);
   }
+}
+
+struct FoldArgs {
+  const Slot* slots;     // this rank's arena: Slot[np][2]
+  int np, par;
+  unsigned long long stamp;
+  int owner[kStar];      // rank holding each star value
+  int rescale;
+  IterScalars* sc;       // this iteration's scalars
+  Acc* acc;              // this iteration's accumulators (reset)
+  double dx, dy, dz, cfl;
+  cav_fluid_params fl;
+  cav_stencil_params sp;
+  BetaFast bf;
+  unsigned long long* err_sticky;
+  const int* abort;
+};
+
+constexpr int kFoldThreads = 128;
+
+__global__ void __launch_bounds__(kFoldThreads) k_fold(const FoldArgs a) {
+  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
+  __shared__ unsigned long long sd[3][kFoldThreads], se[kFoldThreads];
+  const int t = threadIdx.x;
   unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
-  __syncthreads();
-  if (tid == 0) dbg_stamp(a.dbg, kDbgSyncPush, a.n);
-  const bool failed = *reinterpret_cast<volatile unsigned long long*>(a.timeout_flag) != ~0ull;
-  for (int r = tid; r < a.np; r += kSyncThreads) {
-    const Slot* s = a.my_slots + (r * 2 + par);
-    const unsigned long long t0 = globaltimer_ns();
-    while (!failed && ld_acquire_sys(&s->stamp) < static_cast<unsigned long long>(a.n) + 1) {
-      if (globaltimer_ns() - t0 > a.timeout_ns) {
-        atomicMin(a.timeout_flag, err_code(a.n, r, 15));
-        break;
-      }
-      __nanosleep(32);
-    }
+  for (int r = t; r < a.np; r += kFoldThreads) {
+    const Slot* s = a.slots + (r * 2 + a.par);
+    if (ld_acquire_sys(&s->stamp) < a.stamp) continue;  // only after an abort released the wait
     d0 = max(d0, __ldcg(&s->d[0]));
     d1 = max(d1, __ldcg(&s->d[1]));
     d2 = max(d2, __ldcg(&s->d[2]));
     e = min(e, __ldcg(&s->err));
-    if (r == a.owner) spc = __ldcg(&s->pc);
   }
-  sd[0][tid] = d0;
-  sd[1][tid] = d1;
-  sd[2][tid] = d2;
-  se[tid] = e;
+  sd[0][t] = d0;
+  sd[1][t] = d1;
+  sd[2][t] = d2;
+  se[t] = e;
   __syncthreads();
-  if (tid == 0) {
-    for (int t = 1; t < kSyncThreads; ++t) {
-      d0 = max(d0, sd[0][t]);
-      d1 = max(d1, sd[1][t]);
-      d2 = max(d2, sd[2][t]);
-      e = min(e, se[t]);
-    }
-    const unsigned long long dm[3] = {d0, d1, d2};
-    a.sc_next->dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, a.fl, a.cfl);
-    a.sc_next->pc = (a.rescale && a.n >= 1) ? spc : 0.0;
-    if (e < *a.err_sticky) *a.err_sticky = e;
-    Acc z{};
-    z.err = ~0ull;
-    *a.acc_next = z;
-    dbg_stamp(a.dbg, kDbgSyncDone, a.n);
+  if (t != 0) return;
+  for (int q = 1; q < kFoldThreads; ++q) {
+    d0 = max(d0, sd[0][q]);
+    d1 = max(d1, sd[1][q]);
+    d2 = max(d2, sd[2][q]);
+    e = min(e, se[q]);
   }
+  const unsigned long long dm[3] = {d0, d1, d2};
+  const double dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, a.fl, a.cfl);
+  double pcs = 0.0;
+  if (a.rescale) {
+    double v[kStar];
+    for (int q = 0; q < kStar; ++q) v[q] = __ldcg(&a.slots[a.owner[q] * 2 + a.par].star[q]);
+    Star s{};
+    s.p = v[0];
+    s.pxm = v[1];
+    s.pxp = v[2];
+    s.pxm2 = v[3];
+    s.pxp2 = v[4];
+    s.pym = v[5];
+    s.pyp = v[6];
+    s.pym2 = v[7];
+    s.pyp2 = v[8];
+    s.pzm = v[9];
+    s.pzp = v[10];
+    s.pzm2 = v[11];
+    s.pzp2 = v[12];
+    s.u = v[13];
+    s.uxm = v[14];
+    s.uxp = v[15];
+    s.v = v[16];
+    s.vym = v[17];
+    s.vyp = v[18];
+    s.w = v[19];
+    s.wzm = v[20];
+    s.wzp = v[21];
+    // center_p_update's arithmetic (R_p reads only these values)
+    pcs = s.p + dt * residual_of(s, a.sp, a.bf).p;
+  }
+  a.sc->dt = dt;
+  a.sc->pc = 0.0;
+  a.sc->pcs = pcs;
+  Acc z{};
+  z.err = ~0ull;
+  *a.acc = z;
+  if (e < *a.err_sticky) *a.err_sticky = e;
 }
 
 // Whole-storage export in the reference Field3 layout: interior from `cur`
@@ -709,14 +404,19 @@ struct ConvState {
 // (ReproSum, inc/util/repro_sum.hpp; residual_norm_partials,
 // src/solver.cpp:259-274). Each thread walks one k-segment of one (i,j)
 // column (coalesced across a warp), so its consecutive terms are z-neighbours
-// and the runs stay long, as in the step kernel.
+// and the runs stay long, as in the step kernel. It also takes the L-inf
+// norm, max |R_v| over the interior: an exact, order-free maximum of the
+// magnitudes' bit patterns.
 constexpr int kNormRunThreads = 256, kNormRunSeg = 128;
+static_assert(kNormRunSeg <= 4096, "a digit run of up to kNormRunSeg terms must fit its 96 bits");
 __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs, Geo g, cav_box b,
                                                                unsigned long long* dig,
                                                                unsigned long long* err_sticky, long long n,
-                                                               int rank) {
-  __shared__ unsigned long long sd[5 * kDigits];
+                                                               int rank, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  __shared__ unsigned long long sd[5 * kDigits], smx[5];
   for (int x = threadIdx.x; x < 5 * kDigits; x += kNormRunThreads) sd[x] = 0;
+  if (threadIdx.x < 5) smx[threadIdx.x] = 0;
   __syncthreads();
   const int bw = b.hi[0] - b.lo[0], bh = b.hi[1] - b.lo[1];
   const long long col = static_cast<long long>(blockIdx.x) * kNormRunThreads + threadIdx.x;
@@ -725,6 +425,7 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
   unsigned nf = 0;
   if (col < static_cast<long long>(bw) * bh * ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg)) {
     DigitRun runs[5];
+    unsigned long long mx[5] = {0, 0, 0, 0, 0};
     for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
     const long long fs = g.fstride, plane = static_cast<long long>(g.pitch) * g.ypitch;
     const int k1 = min(k0 + kNormRunSeg, b.hi[2]);
@@ -735,36 +436,43 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
       for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + v * fs);
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
+        mx[v] = max(mx[v], abs_bits(x[v]));
         const double x2 = x[v] * x[v];
         if (nonfinite(x2)) nf = 1;
         else digit_run_add(runs[v], sd + v * kDigits, x2);
       }
     }
 #pragma unroll
-    for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sd + v * kDigits);
+    for (int v = 0; v < 5; ++v) {
+      digit_run_flush(runs[v], sd + v * kDigits);
+      mx[v] = warp_max_u64(mx[v]);
+      if ((threadIdx.x & 31) == 0 && mx[v]) atomicMax(&smx[v], mx[v]);
+    }
   }
   __syncthreads();
   for (int x = threadIdx.x; x < 5 * kDigits; x += kNormRunThreads)
     if (sd[x]) atomicAdd(&dig[x], sd[x]);
+  if (threadIdx.x < 5 && smx[threadIdx.x]) atomicMax(&dig[5 * kDigits + threadIdx.x], smx[threadIdx.x]);
   if (nf) atomicMin(err_sticky, err_code(n, rank, 0));  // the step kernel's non-finite norm error
 }
 
 void launch_norm_runs(const double* rs, const Geo& g, const cav_box& b, unsigned long long* dig,
-                      unsigned long long* err, long long n, int rank, cudaStream_t st) {
+                      unsigned long long* err, long long n, int rank, const int* stop, cudaStream_t st) {
   const long long cols = static_cast<long long>(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) *
                          ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg);
   k_norm_runs<<<static_cast<unsigned>((cols + kNormRunThreads - 1) / kNormRunThreads), kNormRunThreads, 0, st>>>(
-      rs, g, b, dig, err, n, rank);
+      rs, g, b, dig, err, n, rank, stop);
   CAV_CUDA(cudaGetLastError());
 }
 
 // The y and z wall ghosts a stored-ghost step reads (p both layers, u,v,w,T
-// the first), of a single-rank state after a step whose wall lanes stored the
-// x ghosts: k_bc's expressions (apply_boundary_conditions, src/solver.cpp:
+// the first), of a state after a step whose wall lanes stored the x ghosts
+// (joined faces are skipped; their ghosts come from the exchange): k_bc's expressions (apply_boundary_conditions, src/solver.cpp:
 // 158-191) with no pending shift. One block row per (face, transverse index),
 // threads along i: coalesced rows, no face search or 64-bit division.
 constexpr int kGhostThreads = 128;
-__global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz(double* s, Geo g, WallInfo w) {
+__global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz(double* s, Geo g, WallInfo w, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   const int face = 2 + static_cast<int>(blockIdx.z);
   if (!w.wall[face]) return;
   const int ax = face >> 1, hi = face & 1;
@@ -803,11 +511,22 @@ __global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long l
   }
 }
 
-// pcs_1 = p'(centre) of the first step (eager mode; later ones are folded by
-// the step kernel's last CTA).
-__global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, BetaFast bf,
-                             IterScalars* sc, int cx, int cy, int cz) {
-  if (threadIdx.x == 0) sc->pcs = center_p_update(state, g, w, sp, bf, sc->dt, 0.0, cx, cy, cz);
+// Scalars of iteration 1 on a single-rank block (later ones are folded by the
+// step kernel's last CTA): dt_1 from the initial state's scan maxima
+// (acc[0]), pcs_1 = p'(centre) of the first step, acc[1] reset.
+__global__ void k_center_pcs(const double* state, Geo g, WallInfo w, cav_stencil_params sp, BetaFast bf, Acc* acc,
+                             IterScalars* sc, double dx, double dy, double dz, double cfl, cav_fluid_params fl,
+                             int rescale, unsigned long long* err_sticky, int cx, int cy, int cz) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long dm[3] = {acc[0].dmax[0], acc[0].dmax[1], acc[0].dmax[2]};
+  const double dt = ops::dt_from_maxima(dm, dx, dy, dz, fl, cfl);
+  sc->dt = dt;
+  sc->pc = 0.0;
+  sc->pcs = rescale ? center_p_update(state, g, w, sp, bf, dt, 0.0, cx, cy, cz) : 0.0;
+  if (acc[0].err < *err_sticky) *err_sticky = acc[0].err;
+  Acc z{};
+  z.err = ~0ull;
+  acc[1] = z;
 }
 
 int getenv_int(const char* name, int dflt) {
@@ -848,14 +567,11 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw
   return m;
 }
 
-// TMA step variants (tile height, ring depth, CTAs per SM); CAV_TMA_CFG picks
-// one for experiments, variant 0 is the default.
-using TmaV0 = TmaCfg<8, 7, 2>;  // default: 2 CTAs x (8 consumer + 1 issuer warps) per SM
-using TmaV1 = TmaCfg<12, 10, 1>;
-using TmaV2 = TmaCfg<8, 14, 1>;
-using TmaV3 = TmaCfg<16, 8, 1>;
-constexpr int kTmaVariants = 4;
-constexpr int kTmaVariantTY[kTmaVariants] = {TmaV0::TY, TmaV1::TY, TmaV2::TY, TmaV3::TY};
+// The step configuration: 32 x 8 tiles (8 consumer warps + 1 TMA issuer warp),
+// a 7-slot ring, 2 CTAs per SM. The measured alternatives (other tile
+// heights, ring depths, 1 CTA per SM) are listed in DESIGN.md §3.
+using TmaV0 = TmaCfg<8, 7, 2>;
+constexpr int kTY = TmaV0::TY;
 
 template <class Cfg, bool NORMS, bool G>
 void tma_attrs() {
@@ -891,6 +607,44 @@ void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool gho
   CAV_CUDA(cudaGetLastError());
 }
 
+// Stream memory operations (driver API): a stream waits for a 64-bit value in
+// device memory to reach a target without occupying any SM, so cross-rank
+// waits survive kernel serialisation (profilers, sanitizers, ranks sharing a
+// GPU) and can sit on a second stream next to the compute stream.
+PFN_cuStreamBatchMemOp_v11070 batch_memop() {
+  static PFN_cuStreamBatchMemOp_v11070 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CAV_CUDA(cudaGetDriverEntryPointByVersion("cuStreamBatchMemOp", &p, 11070, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuStreamBatchMemOp unavailable");
+    fn = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(p);
+  }
+  return fn;
+}
+
+// Waits on `st` until every address holds a value >= its target.
+void stream_wait_geq(cudaStream_t st, const std::vector<std::pair<const unsigned long long*, unsigned long long>>& w,
+                     unsigned flags) {
+  if (w.empty()) return;
+  std::vector<CUstreamBatchMemOpParams> ops(w.size());
+  for (size_t q = 0; q < w.size(); ++q) {
+    std::memset(&ops[q], 0, sizeof ops[q]);
+    ops[q].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+    ops[q].waitValue.address = reinterpret_cast<CUdeviceptr>(w[q].first);
+    ops[q].waitValue.value64 = w[q].second;
+    ops[q].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ | flags;
+  }
+  for (size_t q = 0; q < ops.size(); q += 256) {  // the driver's per-call limit
+    const unsigned cnt = static_cast<unsigned>(std::min<size_t>(256, ops.size() - q));
+    const CUresult r = batch_memop()(reinterpret_cast<CUstream>(st), cnt, ops.data() + q, 0);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamBatchMemOp failed: " + std::to_string(static_cast<int>(r)));
+  }
+}
+
+// counters[] words
+constexpr int kCtrAbort = 60, kCtrWork = 62, kCtrDone = 63;
+
 struct Block {
   cav_block_desc d{};
   std::array<int, 3> gn{}, dims{}, n{};
@@ -903,8 +657,8 @@ struct Block {
   cav_stencil_params sp{};
   Geo g{};
   double* state[2]{};
-  double* staging = nullptr;  // 5 * S doubles in the host Field3 layout (upload / download)
-  double* rscratch = nullptr;  // stored-ghost norm iterations: residuals (state layout), allocated on first use
+  double* staging = nullptr;   // 5 * S doubles in the host Field3 layout (upload / download)
+  double* rscratch = nullptr;  // stored-ghost norm iterations: residuals (state layout)
   bool step_used_scratch = false;  // the last step kernel left its residuals in rscratch
   int cur = 0;
   std::vector<cav_plan_entry> plan;
@@ -912,15 +666,12 @@ struct Block {
   unsigned char* arena = nullptr;
   std::vector<unsigned char*> peer_arena;
   std::vector<bool> peer_ipc;
-  cav_box internal{};
-  std::vector<cav_box> shells;
   // device bookkeeping
   Acc* acc = nullptr;            // [2]
   IterScalars* sc = nullptr;     // [2]
   unsigned long long* err = nullptr;      // sticky min error code
-  unsigned long long* tflag = nullptr;    // timeout code
-  unsigned long long* dbg = nullptr;      // progress stamps
-  unsigned* counters = nullptr;
+  unsigned* counters = nullptr;  // [0, 32) pack entry counters; kCtrAbort, kCtrWork, kCtrDone
+  int* abort_flag = nullptr;     // set (host) when a transport timeout aborts the block
   MsgDesc* d_pack = nullptr;
   MsgDesc* d_unpack = nullptr;
   Slot** d_peer_slots = nullptr;
@@ -931,35 +682,56 @@ struct Block {
   bool ready = false;
   long long next_n = 1;
   bool primed = false;
-  cudaStream_t s0 = nullptr, s1 = nullptr;
+  unsigned long long gen = 0;   // run generation (kGenShift)
+  bool dead = false;            // aborted by a transport timeout
+  unsigned wait_flags = 0;      // CU_STREAM_WAIT_VALUE_FLUSH where supported
+  cudaStream_t s0 = nullptr, s1 = nullptr, saux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_a = nullptr, ev_b = nullptr;
-  std::vector<cudaEvent_t> kev;  // bench: per-step kernel timing
-  int kind_ty = 8;
-  int kchunk = 0;
+  // host-side progress window (np > 1): at most kWindow iterations in flight,
+  // iteration q's completion event at win[q % kWindow]
+  static constexpr int kWindow = 12;
+  cudaEvent_t win[kWindow]{};
+  long long win_it[kWindow]{};
+  // bench timing per iteration: e[0], e[1] around the wait for the peers'
+  // scalars; e[2..] pairs around the step launches; e_join after the halo join
+  struct IterTiming {
+    cudaEvent_t e[7];
+  };
+  std::vector<IterTiming> timing;
+  size_t timing_used = 0;
   CUtensorMap tmap[2][2];  // [state][p, uvwT]
   BetaFast bf{-1.0, 0u};
-  bool eager = false;            // single-rank TMA pipeline: rescaled p stored directly
-  bool ghosts = false;           // eager pipeline with stored wall ghosts (see launch_step)
-  bool ghost_writes = true;     // CAV_GHOST_WRITES=0: always k_bc
-  bool step_wrote_ghosts = false;  // the last step kernel wrote its output's wall ghosts itself
+  bool ghosts = false;           // stored wall ghosts (see launch_step)
+  bool ghost_writes = true;      // CAV_GHOST_WRITES=0: always k_bc
+  bool step_wrote_ghosts = false;  // the last step kernel wrote its output's x-wall ghosts itself
   int tail_chunks = -1;          // CAV_TAIL_CHUNKS: short chunks at the end (-1 = two waves)
   int tma_chunk = 0;             // CAV_TMA_CHUNK: fixed k-chunk (0 = balanced choice)
   WallInfo winfo{};
   int tma_grid = 0;
-  int tma_variant = 0;
-  bool two_streams = false;  // CAV_OVERLAP_STREAMS=2
+  int shell[4] = {0, 0, 0, 0};   // internal tile range sx0, sx1, sy0, sy1
+  int zsh[2] = {0, 0};           // joined low / high z faces
+  StarCells star_mine{};
+  int star_owner[kStar]{};
   double host_marks[6] = {};  // diagnostics: host timestamps inside the first run (s)
-  bool use_tma = true;
 
   explicit Block(const cav_block_desc& desc);
   ~Block();
   double* field(int s, int v) const { return state[s] + v * g.fstride; }
+  unsigned long long base() const { return gen << kGenShift; }
   void ensure_ready();
   void prologue();
-  void iteration(long long it, bool check, unsigned long long* dig, bool timed_kernel);
-  void launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig);
-  void launch_shells(long long it, bool check, unsigned long long* dig);
+  void iteration(long long it, bool check, unsigned long long* dig, IterTiming* tm);
+  void launch_step(int part, long long it, bool check, unsigned long long* dig);
+  void launch_fold(long long it);
+  void launch_push(long long it);
+  void launch_ghosts();
   void update_ledger(cav_ledger& l) const;
+  // np > 1: keeps at most kWindow iterations in flight; polls with the
+  // transport timeout (a missing peer raises TransportTimeout, not a hang)
+  void window_mark(long long it);
+  void window_drain();
+  void wait_event(cudaEvent_t e);
+  [[noreturn]] void on_timeout();
 };
 
 Block::Block(const cav_block_desc& desc) : d(desc) {
@@ -991,20 +763,12 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   sp = host::stencil_params(dx, dy, dz, d.fluid);
   bf = host::beta_fast(sp.u_ref);
   plan = host::build_plan(n, rank_at, d.strategy);
-  host::overlap_regions(n, rank_at, &internal, shells);
   lay = arena_layout(plan, d.np);
 
   CAV_CUDA(cudaSetDevice(d.device));
-  {
-    // The comm stream may run at high priority (CAV_COMM_PRIORITY=1) so its
-    // small kernels win CTA slots; default is equal priority.
-    int lo, hi;
-    CAV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const char* pr = std::getenv("CAV_COMM_PRIORITY");
-    const bool high = pr && std::atoi(pr) != 0;
-    CAV_CUDA(cudaStreamCreateWithPriority(&s0, cudaStreamNonBlocking, lo));
-    CAV_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, high ? hi : lo));
-  }
+  CAV_CUDA(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+  CAV_CUDA(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  CAV_CUDA(cudaStreamCreateWithFlags(&saux, cudaStreamNonBlocking));
   // padded layout: interior rows start 128-byte aligned (off 14 -> i=2 at 16)
   g.nx = n[0];
   g.ny = n[1];
@@ -1013,6 +777,30 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   g.pitch = static_cast<int>(align_up(static_cast<size_t>(g.off + n[0] + 4), 16));
   g.ypitch = n[1] + 4;
   g.fstride = static_cast<long long>(align_up(static_cast<size_t>(g.pitch) * g.ypitch * (n[2] + 4), 32));
+
+  // the centre cell's stencil values this rank owns (k_push) and the owner of
+  // each (k_fold); the centre of a valid grid (>= 5 nodes per axis) is at
+  // least two nodes from every wall, so its stencil has no wall ghosts
+  {
+    static const int off[kStar][4] = {{0, 0, 0, 0},  {0, -1, 0, 0}, {0, 1, 0, 0},  {0, -2, 0, 0}, {0, 2, 0, 0},
+                                      {0, 0, -1, 0}, {0, 0, 1, 0},  {0, 0, -2, 0}, {0, 0, 2, 0},  {0, 0, 0, -1},
+                                      {0, 0, 0, 1},  {0, 0, 0, -2}, {0, 0, 0, 2},  {1, 0, 0, 0},  {1, -1, 0, 0},
+                                      {1, 1, 0, 0},  {2, 0, 0, 0},  {2, 0, -1, 0}, {2, 0, 1, 0},  {3, 0, 0, 0},
+                                      {3, 0, 0, -1}, {3, 0, 0, 1}};
+    for (int q = 0; q < kStar; ++q) {
+      const std::array<int, 3> cell{c[0] + off[q][1], c[1] + off[q][2], c[2] + off[q][3]};
+      for (int a = 0; a < 3; ++a)
+        if (cell[a] < 0 || cell[a] >= gn[a]) throw std::invalid_argument("block: centre stencil reaches a wall");
+      star_owner[q] = host::owner_of(ext, cell);
+      if (star_owner[q] == d.rank) {
+        const int m = star_mine.n++;
+        star_mine.slot[m] = q;
+        star_mine.var[m] = off[q][0];
+        star_mine.idx[m] = g.idx(cell[0] - e.lo[0] + 2, cell[1] - e.lo[1] + 2, cell[2] - e.lo[2] + 2);
+      }
+    }
+  }
+
   for (int s = 0; s < 2; ++s) {
     CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
     CAV_CUDA(cudaMemsetAsync(state[s], 0, 5 * g.fstride * sizeof(double), s0));
@@ -1023,61 +811,67 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   {  // load every kernel module now (see ops::preload_kernels)
     ops::preload_kernels();
     cudaFuncAttributes fa;
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, false>));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tiled<8, true>));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<false>));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_shells<true>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_pack));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_wait_flags));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_unpack));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_scalar_sync));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_push));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_fold));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_import));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_center_pcs));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_conv_check));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_norm_runs));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_ghosts_yz));
   }
   {
-    const char* k = std::getenv("CAV_STEP_KERNEL");
-    use_tma = !(k && std::string(k) == "tiled");
     tail_chunks = getenv_int("CAV_TAIL_CHUNKS", -1);
     tma_chunk = getenv_int("CAV_TMA_CHUNK", 0);
-    const char* ea = std::getenv("CAV_EAGER");
-    eager = use_tma && d.np == 1 && !(ea && std::atoi(ea) == 0);
     // stored ghosts pay from about 150^3 (measured per iteration: 32^3 14.6
     // vs 10.3 us, 128^3 62.1 vs 60.7 us, 256^3 321 vs 335 us): below that the
     // extra ghost-kernel launch costs more than the single accessor saves
     const int sg = getenv_int("CAV_STORED_GHOSTS", -1);
-    ghosts = eager && (sg == 1 || (sg < 0 && static_cast<long long>(n[0]) * n[1] * n[2] >= 3000000LL));
+    ghosts = sg == 1 || (sg < 0 && static_cast<long long>(n[0]) * n[1] * n[2] >= 3000000LL);
     ghost_writes = getenv_int("CAV_GHOST_WRITES", 1) != 0;
-    const char* os = std::getenv("CAV_OVERLAP_STREAMS");
-    two_streams = os && std::atoi(os) == 2;
-    const char* v = std::getenv("CAV_TMA_CFG");
-    tma_variant = v ? std::max(0, std::min(kTmaVariants - 1, std::atoi(v))) : 0;
-    switch (tma_variant) {
-      case 1: tma_grid = tma_setup<TmaV1>(d.device); break;
-      case 2: tma_grid = tma_setup<TmaV2>(d.device); break;
-      case 3: tma_grid = tma_setup<TmaV3>(d.device); break;
-      default: tma_grid = tma_setup<TmaV0>(d.device); break;
-    }
-    const int ty = kTmaVariantTY[tma_variant];
+    tma_grid = tma_setup<TmaV0>(d.device);
     for (int s = 0; s < 2; ++s) {
-      tmap[s][0] = make_state_map(state[s], g, 1, kPW, ty + 4);
-      tmap[s][1] = make_state_map(state[s] + g.fstride, g, 4, kQW, ty + 2);
+      tmap[s][0] = make_state_map(state[s], g, 1, kPW, kTY + 4);
+      tmap[s][1] = make_state_map(state[s] + g.fstride, g, 4, kQW, kTY + 2);
     }
+    // internal / shell tiles (overlap): a tile is internal unless it holds
+    // one of the two cell layers next to a joined face
+    const int tx = (n[0] + 31) / 32, ty = (n[1] + kTY - 1) / kTY;
+    shell[0] = walls[0] ? 0 : 1;
+    shell[1] = walls[1] ? tx : (n[0] - 2) / 32;
+    shell[2] = walls[2] ? 0 : 1;
+    shell[3] = walls[3] ? ty : (n[1] - 2) / kTY;
+    if (shell[1] < shell[0]) shell[1] = shell[0];
+    if (shell[3] < shell[2]) shell[3] = shell[2];
+    zsh[0] = walls[4] ? 0 : 1;
+    zsh[1] = walls[5] ? 0 : 1;
+  }
+  if (ghosts) {  // residual scratch of norm iterations, allocated up front (not inside the loop)
+    CAV_CUDA(cudaMalloc(&rscratch, 5 * static_cast<size_t>(g.fstride) * sizeof(double)));
+  }
+  if (d.np > 1) {
+    int dev = 0;
+    CAV_CUDA(cudaGetDevice(&dev));
+    int ok64 = 0, flush = 0;
+    CAV_CUDA(cudaDeviceGetAttribute(&ok64, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS),
+                                    dev));
+    if (!ok64) throw CudaError("block: the device does not support 64-bit stream memory operations");
+    CAV_CUDA(cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES),
+                                    dev));
+    wait_flags = flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0;
+    batch_memop();
   }
   CAV_CUDA(cudaMalloc(&arena, lay.bytes));
-  // Stream-ordered and completed before any peer can see this arena: a
-  // legacy-stream cudaMemset is not ordered against the non-blocking streams
-  // of other ranks and could wipe a flag a fast peer already wrote.
+  // Stream-ordered and completed before any peer can see this arena.
   CAV_CUDA(cudaMemsetAsync(arena, 0, lay.bytes, s0));
   CAV_CUDA(cudaMalloc(&acc, 2 * sizeof(Acc)));
   CAV_CUDA(cudaMalloc(&sc, 2 * sizeof(IterScalars)));
   CAV_CUDA(cudaMalloc(&err, 2 * sizeof(unsigned long long)));
-  tflag = err + 1;
-  CAV_CUDA(cudaMalloc(&dbg, kDbgStages * sizeof(unsigned long long)));
-  CAV_CUDA(cudaMemsetAsync(dbg, 0, kDbgStages * sizeof(unsigned long long), s0));
   CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
+  abort_flag = reinterpret_cast<int*>(counters + kCtrAbort);
   CAV_CUDA(cudaMalloc(&conv, sizeof(ConvState)));
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
@@ -1087,6 +881,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   }
   CAV_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   CAV_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  for (auto& w : win) CAV_CUDA(cudaEventCreateWithFlags(&w, cudaEventDisableTiming));
   ev_a = make_event();
   ev_b = make_event();
   CAV_CUDA(cudaStreamSynchronize(s0));
@@ -1101,7 +896,10 @@ Block::~Block() {
   if (s1) cudaStreamSynchronize(s1);
   for (int r = 0; r < d.np; ++r)
     if (peer_ipc[r] && peer_arena[r]) cudaIpcCloseMemHandle(peer_arena[r]);
-  for (auto e : kev) cudaEventDestroy(e);
+  for (auto& t : timing)
+    for (auto e : t.e) cudaEventDestroy(e);
+  for (auto w : win)
+    if (w) cudaEventDestroy(w);
   cudaFree(state[0]);
   cudaFree(state[1]);
   cudaFree(staging);
@@ -1112,7 +910,6 @@ Block::~Block() {
   cudaFree(err);
   cudaFree(counters);
   cudaFree(conv);
-  cudaFree(dbg);
   cudaFree(d_peer_slots);
   cudaFree(d_pack);
   cudaFree(d_unpack);
@@ -1124,9 +921,11 @@ Block::~Block() {
   if (ev_b) cudaEventDestroy(ev_b);
   if (s0) cudaStreamDestroy(s0);
   if (s1) cudaStreamDestroy(s1);
+  if (saux) cudaStreamDestroy(saux);
 }
 
 void Block::ensure_ready() {
+  if (dead) throw std::logic_error("block: aborted by an earlier transport timeout");
   if (ready) return;
   for (int r = 0; r < d.np; ++r)
     if (!peer_arena[r])
@@ -1172,16 +971,11 @@ void Block::ensure_ready() {
     CAV_CUDA(cudaMemcpyAsync(d_unpack, up.data(), up.size() * sizeof(MsgDesc), cudaMemcpyHostToDevice, s0));
   }
   CAV_CUDA(cudaStreamSynchronize(s0));
-  // tile shape: 32 x 8 threads, k split so the grid fills ~2 waves of 148 SMs
-  const long long tiles = ((n[0] + 31) / 32) * static_cast<long long>((n[1] + 7) / 8);
-  const long long want = 148 * 4;
-  int chunks = static_cast<int>(std::max<long long>(1, (want + tiles - 1) / tiles));
-  chunks = std::min(chunks, std::max(1, n[2] / 16));
-  kchunk = (n[2] + chunks - 1) / chunks;
   ready = true;
 }
 
 void Block::prologue() {
+  ++gen;
   Acc z[2] = {};
   z[0].err = z[1].err = ~0ull;
   CAV_CUDA(cudaMemcpyAsync(acc, z, sizeof z, cudaMemcpyHostToDevice, s0));
@@ -1191,128 +985,78 @@ void Block::prologue() {
   const cav_field_ptrs f{field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
   const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
   ops::launch_dt_scan(f, g, ib, sp.u_ref, acc, 1, d.rank, s0);  // dt_1 from the initial state
-  SyncArgs a{};
-  a.dbg = dbg;
-  a.acc_cur = acc;
-  a.acc_next = acc + 1;
-  a.sc_next = sc + 1;
-  a.my_slots = reinterpret_cast<Slot*>(arena + lay.slots);
-  a.peer_slots = d_peer_slots;
+  if (ghosts) {  // the first input state's wall ghosts (stored-ghost step)
+    double* fc[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
+    ops::launch_bc(fc, g, walls, d.fluid, nullptr, s0);
+  }
+  if (d.np == 1) {
+    // scalars of iteration 1 directly: dt_1 (the fold of the scan's maxima)
+    // and pcs_1 = p'(centre) of the first step
+    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, acc, sc + 1, dx, dy, dz, d.cfl, d.fluid,
+                                   d.rescale, err, cx, cy, cz);
+    CAV_CUDA(cudaGetLastError());
+  } else {
+    launch_push(0);  // iteration 0's maxima (the scan) and the initial state's centre star
+  }
+  primed = true;
+}
+
+void Block::launch_fold(long long it) {
+  // every rank's push of iteration it-1
+  const int par = static_cast<int>((it - 1) & 1);
+  const unsigned long long want = base() + static_cast<unsigned long long>(it);
+  Slot* mine = reinterpret_cast<Slot*>(arena + lay.slots);
+  std::vector<std::pair<const unsigned long long*, unsigned long long>> w;
+  for (int r = 0; r < d.np; ++r) w.emplace_back(&mine[r * 2 + par].stamp, want);
+  stream_wait_geq(s0, w, wait_flags);
+  FoldArgs a{};
+  a.slots = mine;
   a.np = d.np;
-  a.rank = d.rank;
-  a.owner = owner;
-  a.n = 0;
+  a.par = par;
+  a.stamp = want;
+  for (int q = 0; q < kStar; ++q) a.owner[q] = star_owner[q];
+  a.rescale = d.rescale;
+  a.sc = sc + (it & 1);
+  a.acc = acc + (it & 1);
   a.dx = dx;
   a.dy = dy;
   a.dz = dz;
   a.cfl = d.cfl;
   a.fl = d.fluid;
-  a.rescale = d.rescale;
+  a.sp = sp;
+  a.bf = bf;
   a.err_sticky = err;
-  a.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
-  a.timeout_flag = tflag;
-  k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
+  a.abort = abort_flag;
+  k_fold<<<1, kFoldThreads, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
-  if (ghosts) {  // the first input state's wall ghosts (stored-ghost step)
-    double* fc[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
-    ops::launch_bc(fc, g, walls, d.fluid, nullptr, s0);
-  }
-  if (eager && d.rescale) {  // pcs_1 for the first step's store (IterScalars)
-    k_center_pcs<<<1, 32, 0, s0>>>(state[cur], g, winfo, sp, bf, sc + 1, cx, cy, cz);
-    CAV_CUDA(cudaGetLastError());
-  }
-  primed = true;
 }
 
-void Block::launch_step(const cav_box& box, long long it, bool check, unsigned long long* dig) {
+void Block::launch_push(long long it) {
+  PushArgs a{};
+  a.acc = acc + (it & 1);
+  a.state = state[it == 0 ? cur : cur ^ 1];  // S_it: the step's output (the initial state for it == 0)
+  a.fstride = g.fstride;
+  a.mine = star_mine;
+  a.peer_slots = d_peer_slots;
+  a.np = d.np;
+  a.rank = d.rank;
+  a.par = static_cast<int>(it & 1);
+  a.stamp = base() + static_cast<unsigned long long>(it) + 1;
+  a.abort = abort_flag;
+  k_push<<<1, 32, 0, s0>>>(a);
+  CAV_CUDA(cudaGetLastError());
+}
+
+void Block::launch_step(int part, long long it, bool check, unsigned long long* dig) {
   step_used_scratch = false;
-  const long long vol = host::box_volume(box);
-  if (vol == 0) return;
-  // TMA boxes must start 16-byte aligned along x (even FP64 element)
-  if (use_tma && ((g.off + box.lo[0]) & 1) == 0) {
-    TmaStepArgs a{};
-    a.out = state[cur ^ 1];
-    a.g = g;
-    a.sp = sp;
-    a.bf = bf;
-    a.work = counters + 62;
-    a.eager = eager ? 1 : 0;
-    a.stop = stop_flag;
-    a.box = box;
-    a.sc = sc + (it & 1);
-    a.acc = acc + (it & 1);
-    a.digits = dig;
-    a.cx = cx;
-    a.cy = cy;
-    a.cz = cz;
-    a.n = it;
-    a.rank = d.rank;
-    const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
-    a.tiles_x = (bw + 31) / 32;
-    const int ty = kTmaVariantTY[tma_variant];
-    a.ntiles = a.tiles_x * ((bh + ty - 1) / ty);
-    // k-chunk: long items amortise the per-item window restart (4 extra
-    // planes); the dynamic counter balances them and the short tail chunks
-    // below trim the end (measured at 256^3: 48 best of 24..96, +0.6% over 32).
-    // Small boxes get shorter chunks so that there are items for every CTA
-    // (a 32^3 block has 4 tiles: 48-plane items would leave 292 CTAs idle).
-    a.chunk = static_cast<int>(std::max<long long>(
-        1, std::min<long long>(48, static_cast<long long>(bd) * a.ntiles / tma_grid)));
-    a.chunk = std::min(a.chunk, bd);
-    if (tma_chunk > 0) a.chunk = std::min(bd, tma_chunk);  // CAV_TMA_CHUNK (experiments)
-    // tail: about two waves' worth of short items at the end of the order
-    {
-      const int ls = std::max(4, a.chunk / 4);
-      int nsmall = tail_chunks >= 0 ? tail_chunks
-                                    : static_cast<int>((2LL * tma_grid + a.ntiles - 1) / a.ntiles);
-      nsmall = std::min(nsmall, (bd / 2) / ls);  // keep most of the box in long items
-      if (a.chunk <= ls) nsmall = 0;
-      const int bigext = bd - nsmall * ls;
-      a.nbig = (bigext + a.chunk - 1) / a.chunk;
-      a.bigend = box.lo[2] + bigext;
-      a.chunk_tail = ls;
-      a.nchunks = a.nbig + nsmall;
-    }
-    a.walls = winfo;
-    a.fold = d.np == 1 ? 1 : 0;
-    a.done = counters + 63;
-    a.sc_next = sc + ((it + 1) & 1);
-    a.acc_next = acc + ((it + 1) & 1);
-    a.err_sticky = err;
-    a.dx = dx;
-    a.dy = dy;
-    a.dz = dz;
-    a.cfl = d.cfl;
-    a.nu = d.fluid.nu;
-    a.alpha = d.fluid.alpha;
-    a.rescale = d.rescale;
-    // stored ghosts: the step writes its output's x-wall ghosts when the
-    // three interior layers next to each x wall lie in one warp (one 32-wide
-    // tile row); k_ghosts_yz writes the y and z faces after it (k_bc all faces otherwise)
-    a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
-    if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
-      if (!rscratch) CAV_CUDA(cudaMalloc(&rscratch, 5 * static_cast<size_t>(g.fstride) * sizeof(double)));
-      a.rs = rscratch;
-      step_used_scratch = true;
-    }
-    step_wrote_ghosts = a.gw != 0;
-    const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
-    const int grid = static_cast<int>(std::min<long long>(tma_grid, total));
-    switch (tma_variant) {
-      case 1: tma_launch<TmaV1>(tmap[cur], a, check, ghosts, grid, s0); break;
-      case 2: tma_launch<TmaV2>(tmap[cur], a, check, ghosts, grid, s0); break;
-      case 3: tma_launch<TmaV3>(tmap[cur], a, check, ghosts, grid, s0); break;
-      default: tma_launch<TmaV0>(tmap[cur], a, check, ghosts, grid, s0); break;
-    }
-    return;
-  }
-  StepArgs a{};
-  a.in = state[cur];
+  TmaStepArgs a{};
   a.out = state[cur ^ 1];
   a.g = g;
   a.sp = sp;
   a.bf = bf;
-  a.box = box;
+  a.work = counters + kCtrWork;
+  a.stop = d.np > 1 ? abort_flag : stop_flag;
+  a.box = cav_box{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
   a.sc = sc + (it & 1);
   a.acc = acc + (it & 1);
   a.digits = dig;
@@ -1321,161 +1065,167 @@ void Block::launch_step(const cav_box& box, long long it, bool check, unsigned l
   a.cz = cz;
   a.n = it;
   a.rank = d.rank;
-  const int bw = box.hi[0] - box.lo[0], bh = box.hi[1] - box.lo[1], bd = box.hi[2] - box.lo[2];
-  a.kchunk = std::min(kchunk, bd);
-  const dim3 grid((bw + 31) / 32, (bh + 7) / 8, (bd + a.kchunk - 1) / a.kchunk);
-  const dim3 block(32, 8);
-  if (check) k_step_tiled<8, true><<<grid, block, 0, s0>>>(a);
-  else k_step_tiled<8, false><<<grid, block, 0, s0>>>(a);
-  CAV_CUDA(cudaGetLastError());
-}
-
-void Block::launch_shells(long long it, bool check, unsigned long long* dig) {
-  if (shells.empty()) return;
-  ShellArgs a{};
-  a.s.in = state[cur];
-  a.s.out = state[cur ^ 1];
-  a.s.g = g;
-  a.s.sp = sp;
-  a.s.bf = bf;
-  a.s.sc = sc + (it & 1);
-  a.s.acc = acc + (it & 1);
-  a.s.digits = dig;
-  a.s.cx = cx;
-  a.s.cy = cy;
-  a.s.cz = cz;
-  a.s.n = it;
-  a.s.rank = d.rank;
+  const int bw = n[0], bh = n[1], bd = n[2];
+  a.tiles_x = (bw + 31) / 32;
+  a.ntiles = a.tiles_x * ((bh + kTY - 1) / kTY);
+  // z chunks: two-plane shell chunks next to joined z faces (overlap), the
+  // middle in k-chunks. Long items amortise the per-item window restart (4
+  // extra planes); the dynamic counter balances them and the short tail
+  // chunks below trim the end (measured at 256^3: 48 best of 24..96, +0.6%
+  // over 32). Small boxes get shorter chunks so that there are items for
+  // every CTA (a 32^3 block has 4 tiles: 48-plane items would leave 292 CTAs idle).
+  const bool split = d.np > 1 && d.overlap;
+  a.zl = split ? zsh[0] : 0;
+  a.zh = split ? zsh[1] : 0;
+  a.mlo = a.box.lo[2] + 2 * a.zl;
+  const int bm = bd - 2 * (a.zl + a.zh);  // planes in the middle chunks (>= 1: validate_grid needs 5)
+  a.chunk = static_cast<int>(std::max<long long>(
+      1, std::min<long long>(48, static_cast<long long>(bm) * a.ntiles / tma_grid)));
+  a.chunk = std::min(a.chunk, bm);
+  if (tma_chunk > 0) a.chunk = std::min(bm, tma_chunk);  // CAV_TMA_CHUNK (experiments)
+  if (a.chunk > 4096) throw std::invalid_argument("block: k-chunk above 4096 planes (96-bit digit runs)");
+  {  // tail: about two waves' worth of short items at the end of the order
+    const int ls = std::max(4, a.chunk / 4);
+    int nsmall = tail_chunks >= 0 ? tail_chunks : static_cast<int>((2LL * tma_grid + a.ntiles - 1) / a.ntiles);
+    nsmall = std::min(nsmall, (bm / 2) / ls);  // keep most of the box in long items
+    if (a.chunk <= ls) nsmall = 0;
+    const int bigext = bm - nsmall * ls;
+    a.nbig = (bigext + a.chunk - 1) / a.chunk;
+    a.bigend = a.mlo + bigext;
+    a.chunk_tail = ls;
+    a.nchunks = a.zl + a.nbig + nsmall + a.zh;
+  }
+  a.part = split ? part : 0;
+  a.sx0 = shell[0];
+  a.sx1 = shell[1];
+  a.sy0 = shell[2];
+  a.sy1 = shell[3];
   a.walls = winfo;
-  a.nbox = static_cast<int>(shells.size());
-  a.start[0] = 0;
-  for (int b = 0; b < a.nbox; ++b) {
-    a.box[b] = shells[b];
-    a.start[b + 1] = a.start[b] + host::box_volume(shells[b]);
-  }
-  const int nb = static_cast<int>((a.start[a.nbox] + kShellThreads - 1) / kShellThreads);
-  if (check) k_step_shells<true><<<nb, kShellThreads, 0, s0>>>(a);
-  else k_step_shells<false><<<nb, kShellThreads, 0, s0>>>(a);
-  CAV_CUDA(cudaGetLastError());
-}
-
-void Block::iteration(long long it, bool check, unsigned long long* dig, bool timed_kernel) {
-  const IterScalars* sc_n = sc + (it & 1);
-  double* f[5] = {field(cur, 0), field(cur, 1), field(cur, 2), field(cur, 3), field(cur, 4)};
-  if (!use_tma) ops::launch_bc(f, g, walls, d.fluid, sc_n, s0);  // v1 kernel reads stored wall ghosts
-  XArgs x{};
-  x.dbg = dbg;
-  x.state = state[cur];
-  x.g = g;
-  x.n = it;
-  x.sc = sc_n;
-  x.corrupt = d.corrupt_exchange;
-  x.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
-  x.timeout_flag = tflag;
-  x.rank = d.rank;
-  long long maxs = 0;
-  for (const auto& e : plan) maxs = std::max(maxs, e.scalars);
-  const dim3 xgrid(static_cast<unsigned>((maxs + kXThreads * kXItems - 1) / (kXThreads * kXItems)),
-                   static_cast<unsigned>(plan.size()));
-  const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
-  cudaEvent_t* kt = nullptr;
-  if (timed_kernel) {
-    kev.push_back(make_event());
-    kev.push_back(make_event());
-    kt = &kev[kev.size() - 2];
-  }
-  if (plan.empty()) {
-    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
-    launch_step(ib, it, check, dig);
-    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
-    if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, s0);
-  } else if (!d.overlap) {
-    x.msg = d_pack;
-    k_pack<<<xgrid, kXThreads, 0, s0>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    x.msg = d_unpack;
-    k_wait_flags<<<1, 32, 0, s0>>>(x, static_cast<int>(plan.size()));
-    CAV_CUDA(cudaGetLastError());
-    k_unpack<<<xgrid, kXThreads, 0, s0>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
-    launch_step(ib, it, check, dig);
-    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
-  } else if (!two_streams) {
-    // overlap (src/runner.cpp:189-194) in the reference's own order:
-    // exchange_begin (pack = remote stores into the neighbours' slabs),
-    // internal box, exchange_finish (acquire + unpack), external shells. The
-    // neighbours' pushes into our slabs travel while the internal box
-    // computes, so the transfer is hidden without a second stream (and
-    // without cross-stream events, which can serialise ranks sharing a GPU).
-    x.msg = d_pack;
-    k_pack<<<xgrid, kXThreads, 0, s0>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
-    launch_step(internal, it, check, dig);
-    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
-    x.msg = d_unpack;
-    k_wait_flags<<<1, 32, 0, s0>>>(x, static_cast<int>(plan.size()));
-    CAV_CUDA(cudaGetLastError());
-    k_unpack<<<xgrid, kXThreads, 0, s0>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    launch_shells(it, check, dig);
-  } else {
-    // two-stream overlap: pack/wait/unpack on the comm stream concurrently
-    // with the internal box, shells after the join
-    CAV_CUDA(cudaEventRecord(ev_fork, s0));
-    CAV_CUDA(cudaStreamWaitEvent(s1, ev_fork, 0));
-    x.msg = d_pack;
-    k_pack<<<xgrid, kXThreads, 0, s1>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    x.msg = d_unpack;
-    k_wait_flags<<<1, 32, 0, s1>>>(x, static_cast<int>(plan.size()));
-    CAV_CUDA(cudaGetLastError());
-    k_unpack<<<xgrid, kXThreads, 0, s1>>>(x);
-    CAV_CUDA(cudaGetLastError());
-    CAV_CUDA(cudaEventRecord(ev_join, s1));
-    if (kt) CAV_CUDA(cudaEventRecord(kt[0], s0));
-    launch_step(internal, it, check, dig);
-    if (kt) CAV_CUDA(cudaEventRecord(kt[1], s0));
-    CAV_CUDA(cudaStreamWaitEvent(s0, ev_join, 0));
-    launch_shells(it, check, dig);
-  }
-  if (use_tma && d.np == 1) {  // the step kernel's last CTA folded the scalars
-    if (ghosts) {  // wall ghosts of the output state for the next step (eager: no pending shift)
-      double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
-      if (step_wrote_ghosts) {
-        const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
-        k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo);
-        CAV_CUDA(cudaGetLastError());
-      } else {
-        ops::launch_bc(fo, g, walls, d.fluid, nullptr, s0, true);
-      }
-    }
-    cur ^= 1;
-    return;
-  }
-  SyncArgs a{};
-  a.dbg = dbg;
-  a.acc_cur = acc + (it & 1);
-  a.acc_next = acc + ((it + 1) & 1);
+  a.fold = d.np == 1 ? 1 : 0;
+  a.done = counters + kCtrDone;
   a.sc_next = sc + ((it + 1) & 1);
-  a.my_slots = reinterpret_cast<Slot*>(arena + lay.slots);
-  a.peer_slots = d_peer_slots;
-  a.np = d.np;
-  a.rank = d.rank;
-  a.owner = owner;
-  a.n = it;
+  a.acc_next = acc + ((it + 1) & 1);
+  a.err_sticky = err;
   a.dx = dx;
   a.dy = dy;
   a.dz = dz;
   a.cfl = d.cfl;
-  a.fl = d.fluid;
+  a.nu = d.fluid.nu;
+  a.alpha = d.fluid.alpha;
   a.rescale = d.rescale;
-  a.err_sticky = err;
-  a.timeout_ns = static_cast<unsigned long long>(d.timeout_ms * 1e6);
-  a.timeout_flag = tflag;
-  k_scalar_sync<<<1, kSyncThreads, 0, s0>>>(a);
-  CAV_CUDA(cudaGetLastError());
+  // stored ghosts: the step writes its output's x-wall ghosts when the
+  // three interior layers next to each x wall lie in one warp (one 32-wide
+  // tile row); k_ghosts_yz writes the y and z faces after it (k_bc all faces otherwise)
+  a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
+  if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
+    a.rs = rscratch;
+    step_used_scratch = true;
+  }
+  step_wrote_ghosts = a.gw != 0;
+  const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
+  long long wanted = total;
+  if (a.part != 0) {
+    const long long internal = static_cast<long long>(a.nchunks - a.zl - a.zh) * (a.sx1 - a.sx0) * (a.sy1 - a.sy0);
+    wanted = a.part == 1 ? internal : total - internal;
+  }
+  if (wanted <= 0) return;
+  const int grid = static_cast<int>(std::min<long long>(tma_grid, wanted));
+  tma_launch<TmaV0>(tmap[cur], a, check, ghosts, grid, s0);
+}
+
+void Block::launch_ghosts() {
+  if (!ghosts) return;
+  // wall ghosts of the output state for the next step (no pending shift)
+  if (step_wrote_ghosts) {
+    if (!(walls[2] || walls[3] || walls[4] || walls[5])) return;
+    const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
+    k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo, d.np > 1 ? abort_flag : stop_flag);
+    CAV_CUDA(cudaGetLastError());
+  } else {
+    double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
+    ops::launch_bc(fo, g, walls, d.fluid, nullptr, s0, true);
+  }
+}
+
+void Block::iteration(long long it, bool check, unsigned long long* dig, IterTiming* tm) {
+  const cav_box ib{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
+  auto mark = [&](int q, cudaStream_t st) {
+    if (tm) CAV_CUDA(cudaEventRecord(tm->e[q], st));
+  };
+  if (d.np == 1) {  // the step kernel's last CTA folds the scalars
+    mark(0, s0);
+    mark(1, s0);
+    mark(2, s0);
+    launch_step(0, it, check, dig);
+    mark(3, s0);
+    mark(4, s0);
+    mark(5, s0);
+    mark(6, s0);
+    if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, stop_flag, s0);
+    launch_ghosts();
+    cur ^= 1;
+    return;
+  }
+  XArgs x{};
+  x.state = state[cur];
+  x.g = g;
+  x.n = it;
+  x.val = base() + static_cast<unsigned long long>(it);
+  x.corrupt = d.corrupt_exchange;
+  x.abort = abort_flag;
+  long long maxs = 0;
+  for (const auto& e : plan) maxs = std::max(maxs, e.scalars);
+  const dim3 xgrid(static_cast<unsigned>((maxs + kXThreads * kXItems - 1) / (kXThreads * kXItems)),
+                   static_cast<unsigned>(plan.size()));
+  std::vector<std::pair<const unsigned long long*, unsigned long long>> fw;
+  for (size_t m = 0; m < plan.size(); ++m)
+    fw.emplace_back(reinterpret_cast<unsigned long long*>(arena) + m, x.val);
+  // exchange_begin / exchange_finish on stream xs: the pack reads the input
+  // state (complete in s0's order here) and the neighbours' slabs are free
+  // (they passed our scalars of iteration it-2, so they unpacked it-2).
+  const bool ov = d.overlap != 0;
+  cudaStream_t xs = ov ? s1 : s0;
+  if (ov) {
+    CAV_CUDA(cudaEventRecord(ev_fork, s0));
+    CAV_CUDA(cudaStreamWaitEvent(s1, ev_fork, 0));
+  }
+  auto exchange = [&] {
+    if (plan.empty()) return;
+    x.msg = d_pack;
+    k_pack<<<xgrid, kXThreads, 0, xs>>>(x);
+    CAV_CUDA(cudaGetLastError());
+    stream_wait_geq(xs, fw, wait_flags);
+    x.msg = d_unpack;
+    k_unpack<<<xgrid, kXThreads, 0, xs>>>(x);
+    CAV_CUDA(cudaGetLastError());
+  };
+  if (ov) exchange();  // on s1, concurrent with the fold and the internal items
+  mark(0, s0);
+  launch_fold(it);  // waits for every rank's scalars of iteration it-1
+  mark(1, s0);
+  if (ov) {
+    CAV_CUDA(cudaEventRecord(ev_join, s1));
+    // overlap (src/runner.cpp:189-194): internal items while the halos
+    // travel, then the shell items once they landed
+    mark(2, s0);
+    launch_step(1, it, check, dig);
+    mark(3, s0);
+    CAV_CUDA(cudaStreamWaitEvent(s0, ev_join, 0));
+    mark(4, s0);
+    launch_step(2, it, check, dig);
+    mark(5, s0);
+  } else {
+    exchange();
+    mark(2, s0);
+    launch_step(0, it, check, dig);
+    mark(3, s0);
+    mark(4, s0);
+    mark(5, s0);
+  }
+  if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, abort_flag, s0);
+  launch_ghosts();
+  launch_push(it);
+  mark(6, s0);
   cur ^= 1;
 }
 
@@ -1492,6 +1242,85 @@ void Block::update_ledger(cav_ledger& l) const {
     l.bytes_sent += bytes;
     l.messages_sent += 1;
   }
+}
+
+void Block::wait_event(cudaEvent_t e) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const double lim = d.timeout_ms > 0 ? d.timeout_ms : 20000.0;
+  for (int spin = 0;; ++spin) {
+    const cudaError_t r = cudaEventQuery(e);
+    if (r == cudaSuccess) return;
+    if (r != cudaErrorNotReady) CAV_CUDA(r);
+    if (std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() > lim) on_timeout();
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    else std::this_thread::yield();
+  }
+}
+
+void Block::window_mark(long long it) {
+  if (d.np == 1) return;
+  const int q = static_cast<int>(it % kWindow);
+  if (win_it[q] > 0) wait_event(win[q]);  // iteration it - kWindow is complete
+  CAV_CUDA(cudaEventRecord(win[q], s0));
+  win_it[q] = it;
+}
+
+void Block::window_drain() {
+  if (d.np == 1) return;
+  long long last = 0;
+  int lq = -1;
+  for (int q = 0; q < kWindow; ++q)
+    if (win_it[q] > last) {
+      last = win_it[q];
+      lq = q;
+    }
+  if (lq >= 0) wait_event(win[lq]);
+  for (auto& w : win_it) w = 0;
+}
+
+void Block::on_timeout() {
+  // the first iteration that has not completed is the stuck one
+  long long stuck = 0;
+  for (int q = 0; q < kWindow; ++q)
+    if (win_it[q] > 0 && cudaEventQuery(win[q]) != cudaSuccess && (stuck == 0 || win_it[q] < stuck))
+      stuck = win_it[q];
+  cudaGetLastError();
+  if (stuck == 0) stuck = next_n;
+  // what this rank still waits for, read from its arena on the side stream
+  std::vector<unsigned long long> flags(64);
+  std::vector<Slot> slots(2 * d.np);
+  CAV_CUDA(cudaMemcpyAsync(flags.data(), arena, 64 * 8, cudaMemcpyDeviceToHost, saux));
+  CAV_CUDA(cudaMemcpyAsync(slots.data(), arena + lay.slots, slots.size() * sizeof(Slot), cudaMemcpyDeviceToHost, saux));
+  CAV_CUDA(cudaStreamSynchronize(saux));
+  const unsigned long long want = base() + static_cast<unsigned long long>(stuck);
+  std::string out;
+  auto add = [&](int src, int tag) {
+    out += (out.empty() ? "" : ", ");
+    out += "(src=" + std::to_string(src) + ", tag=" + std::to_string(tag) + ")";
+  };
+  for (size_t m = 0; m < plan.size(); ++m)
+    if (flags[m] < want) add(plan[m].neighbor, plan[m].recv_tag);
+  for (int r = 0; r < d.np; ++r)
+    if (r != d.rank && slots[r * 2 + ((stuck - 1) & 1)].stamp < want) add(r, 1001);  // kReduceTag
+  // abort: later kernels return at once; release every wait so the streams drain
+  const int one = 1;
+  CAV_CUDA(cudaMemcpyAsync(abort_flag, &one, sizeof one, cudaMemcpyHostToDevice, saux));
+  const unsigned long long big = ~0ull >> 1;
+  std::vector<unsigned long long> fl(plan.size(), big);
+  if (!fl.empty()) CAV_CUDA(cudaMemcpyAsync(arena, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, saux));
+  for (auto& s : slots) s.stamp = big;
+  for (int r = 0; r < d.np; ++r)
+    for (int p = 0; p < 2; ++p)
+      CAV_CUDA(cudaMemcpyAsync(arena + lay.slots + (r * 2 + p) * sizeof(Slot) + offsetof(Slot, stamp), &big, 8,
+                               cudaMemcpyHostToDevice, saux));
+  CAV_CUDA(cudaStreamSynchronize(saux));
+  cudaStreamSynchronize(s1);
+  cudaStreamSynchronize(s0);
+  cudaGetLastError();
+  dead = true;
+  for (auto& w : win_it) w = 0;
+  throw Timeout("rank " + std::to_string(d.rank) + ": receive timed out at iteration " + std::to_string(stuck) +
+                "; outstanding: " + out);
 }
 
 namespace {
@@ -1621,22 +1450,15 @@ int cav_block_download(cav_block* bh, double* host5) {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
     const long long S = static_cast<long long>(b.n[0] + 4) * (b.n[1] + 4) * (b.n[2] + 4);
-    double pc = 0.0;
-    if (b.primed) {
-      IterScalars s{};
-      CAV_CUDA(cudaMemcpyAsync(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost, b.s0));
-      CAV_CUDA(cudaStreamSynchronize(b.s0));
-      if (b.next_n > 1) pc = s.pc;
-    }
-    if (b.primed && b.next_n > 1 && b.use_tma) {
-      // ghosts the reference's BC stored at the last iteration: recompute them
-      // on the last input state with that iteration's pending shift
+    if (b.primed && b.next_n > 1) {
+      // wall ghosts the reference's BC stored at the last iteration: those of
+      // the last input state (stored states are final, nothing is pending)
       double* fp[5] = {b.field(b.cur ^ 1, 0), b.field(b.cur ^ 1, 1), b.field(b.cur ^ 1, 2), b.field(b.cur ^ 1, 3),
                        b.field(b.cur ^ 1, 4)};
-      ops::launch_bc(fp, b.g, b.walls, b.d.fluid, b.sc + ((b.next_n - 1) & 1), b.s0);
+      ops::launch_bc(fp, b.g, b.walls, b.d.fluid, nullptr, b.s0);
     }
     k_export<<<static_cast<unsigned>((5 * S + 255) / 256), 256, 0, b.s0>>>(b.state[b.cur], b.state[b.cur ^ 1],
-                                                                           b.g, pc, b.staging);
+                                                                           b.g, 0.0, b.staging);
     CAV_CUDA(cudaGetLastError());
     CAV_CUDA(cudaMemcpyAsync(host5, b.staging, 5 * S * sizeof(double), cudaMemcpyDeviceToHost, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
@@ -1645,6 +1467,16 @@ int cav_block_download(cav_block* bh, double* host5) {
 
 static double host_now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// seeded pauses between iterations (cav_block_desc.jitter_seed): perturbs the
+// relative timing of ranks; results must not depend on it
+static void jitter(unsigned long long& st) {
+  if (!st) return;
+  st ^= st << 13;
+  st ^= st >> 7;
+  st ^= st << 17;
+  if ((st & 3) == 0) std::this_thread::sleep_for(std::chrono::microseconds(static_cast<int>((st >> 8) % 400)));
 }
 
 int cav_block_run(cav_block* bh, cav_run_io* io) {
@@ -1666,18 +1498,17 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     long long nchk = 0;
     for (long long it = first; it <= last; ++it) nchk += is_check(it);
     if (nchk > b.digits_cap) {
-      // stream-ordered: cudaFree/cudaMalloc may synchronise the whole device,
-      // which deadlocks against a peer rank's kernel spinning on this GPU
+      // stream-ordered (no device-wide synchronisation while peers run)
       if (b.digits) CAV_CUDA(cudaFreeAsync(b.digits, b.s0));
-      CAV_CUDA(cudaMallocAsync(&b.digits, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
+      CAV_CUDA(cudaMallocAsync(&b.digits, nchk * kNormWords * sizeof(unsigned long long), b.s0));
       b.digits_cap = nchk;
     }
-    if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * 5 * kDigits * sizeof(unsigned long long), b.s0));
+    if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * kNormWords * sizeof(unsigned long long), b.s0));
     if (!b.primed) b.prologue();
     if (mark) b.host_marks[2] = host_now();
-    // device convergence: single-rank fused pipeline only (other ranks' norm
+    // device convergence: single-rank blocks only (other ranks' norm
     // partials would have to be merged first; those runs fold on the host)
-    const bool dconv = io->device_conv && io->want_norms && b.d.np == 1 && b.use_tma && b.eager;
+    const bool dconv = io->device_conv && io->want_norms && b.d.np == 1;
     io->device_conv = dconv ? 1 : 0;
     const int cur0 = b.cur;
     if (dconv) {
@@ -1692,13 +1523,15 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
       started = true;
     }
+    const cav_ledger ledger0 = io->ledger;
+    unsigned long long js = b.d.jitter_seed ? b.d.jitter_seed * 0x9E3779B97F4A7C15ull + b.d.rank + 1 : 0;
     long long ci = 0;
     for (long long it = first; it <= last; ++it) {
       const bool chk = is_check(it);
-      unsigned long long* dig = chk ? b.digits + ci * 5 * kDigits : nullptr;
+      unsigned long long* dig = chk ? b.digits + ci * kNormWords : nullptr;
       if (chk && io->check_iters) io->check_iters[ci] = it;
       ci += chk;
-      b.iteration(it, chk, dig, false);
+      b.iteration(it, chk, dig, nullptr);
       if (dconv && chk) {
         k_conv_check<<<1, 32, 0, b.s0>>>(dig, b.conv, it, io->conv_tol, nglobal);
         CAV_CUDA(cudaGetLastError());
@@ -1709,9 +1542,12 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
         CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
         started = true;
       }
+      b.window_mark(it);
+      jitter(js);
     }
     CAV_CUDA(cudaEventRecord(b.ev_b, b.s0));
     if (mark) b.host_marks[4] = host_now();
+    b.window_drain();
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     if (mark) b.host_marks[5] = host_now();
     float ms = 0.f;
@@ -1732,26 +1568,22 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
         long long kept = 0;
         for (long long q = first; q <= c.it; ++q) kept += is_check(q);
         io->n_checks = nchk = kept;
+        // the reference leaves its loop at the converged iteration: one
+        // exchange per marched iteration, and the timed region ends there
+        // (the no-op tail after it is a few microseconds per iteration)
+        io->ledger = ledger0;
+        for (long long q = first; q <= c.it; ++q) b.update_ledger(io->ledger);
+        if (c.it == 1) io->seconds = 0.0;
       }
     }
     if (nchk && io->norm_digits)
-      CAV_CUDA(cudaMemcpyAsync(io->norm_digits, b.digits, nchk * 5 * kDigits * sizeof(unsigned long long),
+      CAV_CUDA(cudaMemcpyAsync(io->norm_digits, b.digits, nchk * kNormWords * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, b.s0));
     unsigned long long codes[2];
     CAV_CUDA(cudaMemcpyAsync(codes, b.err, sizeof codes, cudaMemcpyDeviceToHost, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     io->err_iteration = 0;
     io->err_kind = 0;
-    if (codes[1] != ~0ull) {
-      const int kind = static_cast<int>(codes[1] & 15);
-      const int who = static_cast<int>((codes[1] >> 4) & 0xFFFFF);
-      const long long tit = static_cast<long long>(codes[1] >> 24);
-      throw Timeout(kind == 15 ? "transport timeout: rank " + std::to_string(b.d.rank) +
-                                     " waiting for scalars from rank " + std::to_string(who) + " at iteration " +
-                                     std::to_string(tit)
-                               : "transport timeout: rank " + std::to_string(b.d.rank) + " waiting on face " +
-                                     std::to_string(kind - 8) + " at iteration " + std::to_string(tit));
-    }
     if (codes[0] != ~0ull && static_cast<long long>(codes[0] >> 24) <= last) {
       io->err_iteration = static_cast<long long>(codes[0] >> 24);
       io->err_kind = static_cast<int>(codes[0] & 15);
@@ -1764,16 +1596,15 @@ int cav_block_debug(cav_block* bh, uint64_t* out, int cap) {
   return guarded([&] {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
-    CAV_CUDA(cudaStreamSynchronize(b.s0));
-    CAV_CUDA(cudaStreamSynchronize(b.s1));
-    std::vector<uint64_t> v(64 + 16 * b.d.np + 2 + 64 + kDbgStages + 6);
-    CAV_CUDA(cudaMemcpy(v.data(), b.arena, (64 + 16 * b.d.np) * 8, cudaMemcpyDeviceToHost));
-    CAV_CUDA(cudaMemcpy(v.data() + 64 + 16 * b.d.np, b.err, 16, cudaMemcpyDeviceToHost));
-    std::vector<unsigned> c(64);
-    CAV_CUDA(cudaMemcpy(c.data(), b.counters, 64 * 4, cudaMemcpyDeviceToHost));
-    for (int q = 0; q < 64; ++q) v[66 + 16 * b.d.np + q] = c[q];
-    CAV_CUDA(cudaMemcpy(v.data() + 130 + 16 * b.d.np, b.dbg, kDbgStages * 8, cudaMemcpyDeviceToHost));
-    std::memcpy(v.data() + 130 + 16 * b.d.np + kDbgStages, b.host_marks, sizeof b.host_marks);
+    // arena flags (64), then per slot (np x 2) its stamp, then the two error codes
+    std::vector<uint64_t> v(64 + 2 * b.d.np + 2);
+    CAV_CUDA(cudaMemcpyAsync(v.data(), b.arena, 64 * 8, cudaMemcpyDeviceToHost, b.saux));
+    std::vector<Slot> sl(2 * b.d.np);
+    CAV_CUDA(cudaMemcpyAsync(sl.data(), b.arena + b.lay.slots, sl.size() * sizeof(Slot), cudaMemcpyDeviceToHost,
+                             b.saux));
+    CAV_CUDA(cudaMemcpyAsync(v.data() + 64 + 2 * b.d.np, b.err, 16, cudaMemcpyDeviceToHost, b.saux));
+    CAV_CUDA(cudaStreamSynchronize(b.saux));
+    for (int q = 0; q < 2 * b.d.np; ++q) v[64 + q] = sl[q].stamp;
     for (size_t q = 0; q < v.size() && static_cast<int>(q) < cap; ++q) out[q] = v[q];
   });
 }
@@ -1782,10 +1613,11 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   Block& b = *bh->b;
   int walls = 0;
   for (int f = 0; f < 6; ++f) walls += b.walls[f];
-  // [bc before the v1 step], step, [bc after the stored-ghost step], [sync]
-  int n = (walls && !b.use_tma ? 1 : 0) + 1 + (walls && b.ghosts ? 1 : 0) + (b.use_tma && b.d.np == 1 ? 0 : 1) +
-          (check && b.ghosts ? 1 : 0);  // [k_norm_runs]
-  if (!b.plan.empty()) n += 3 + (b.d.overlap && !b.shells.empty() ? 1 : 0);  // pack, wait, unpack, [shells]
+  const bool yz = b.walls[2] || b.walls[3] || b.walls[4] || b.walls[5];
+  // step (two launches when overlapping), [ghosts after a stored-ghost step], [k_norm_runs]
+  int n = (b.d.np > 1 && b.d.overlap ? 2 : 1) + (b.ghosts && (yz || !b.ghost_writes) && walls ? 1 : 0) +
+          (check && b.ghosts ? 1 : 0);
+  if (b.d.np > 1) n += 2 + (b.plan.empty() ? 0 : 2);  // fold, push, [pack, unpack]
   return n;
 }
 
@@ -1794,36 +1626,51 @@ int cav_block_scalars(cav_block* bh, double* dt, double* pc) {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
     IterScalars s{};
-    CAV_CUDA(cudaMemcpyAsync(&s, b.sc + (b.next_n & 1), sizeof s, cudaMemcpyDeviceToHost, b.s0));
+    CAV_CUDA(cudaMemcpyAsync(&s, b.sc + ((b.next_n - 1) & 1), sizeof s, cudaMemcpyDeviceToHost, b.s0));
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     *dt = s.dt;
-    *pc = s.pc;
+    *pc = s.pcs;
   });
 }
 
-int cav_block_bench(cav_block* bh, long long n_its, double* total_ms, double* step_ms) {
+int cav_block_bench(cav_block* bh, long long n_its, double out[3]) {
   return guarded([&] {
     Block& b = *bh->b;
     CAV_CUDA(cudaSetDevice(b.d.device));
     b.ensure_ready();
     if (!b.primed) b.prologue();
-    for (auto e : b.kev) cudaEventDestroy(e);
-    b.kev.clear();
+    while (b.timing.size() < static_cast<size_t>(n_its)) {
+      Block::IterTiming t;
+      for (auto& e : t.e) e = make_event();
+      b.timing.push_back(t);
+    }
     CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
-    for (long long k = 0; k < n_its; ++k) b.iteration(b.next_n + k, false, nullptr, true);
+    for (long long k = 0; k < n_its; ++k) {
+      b.iteration(b.next_n + k, false, nullptr, &b.timing[k]);
+      b.window_mark(b.next_n + k);
+    }
     CAV_CUDA(cudaEventRecord(b.ev_b, b.s0));
+    b.window_drain();
     CAV_CUDA(cudaStreamSynchronize(b.s0));
     b.next_n += n_its;
     float ms = 0.f;
     CAV_CUDA(cudaEventElapsedTime(&ms, b.ev_a, b.ev_b));
-    *total_ms = ms;
-    double ks = 0.0;
-    for (size_t q = 0; q + 1 < b.kev.size(); q += 2) {
+    double ks = 0.0, wait = 0.0;
+    for (long long k = 0; k < n_its; ++k) {
+      const auto& e = b.timing[k].e;
       float t = 0.f;
-      CAV_CUDA(cudaEventElapsedTime(&t, b.kev[q], b.kev[q + 1]));
+      CAV_CUDA(cudaEventElapsedTime(&t, e[2], e[3]));
       ks += t;
+      CAV_CUDA(cudaEventElapsedTime(&t, e[4], e[5]));
+      ks += t;
+      CAV_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));  // scalar wait (+ the 1-thread fold)
+      wait += t;
+      CAV_CUDA(cudaEventElapsedTime(&t, e[3], e[4]));  // halo join after the internal items
+      wait += t;
     }
-    *step_ms = n_its ? ks / static_cast<double>(n_its) : 0.0;
+    out[0] = ms;
+    out[1] = n_its ? ks / static_cast<double>(n_its) : 0.0;
+    out[2] = n_its ? wait / static_cast<double>(n_its) : 0.0;
   });
 }
 

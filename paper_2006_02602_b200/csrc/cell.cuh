@@ -211,6 +211,10 @@ struct Geo {
 // split into three 32-bit pieces added to consecutive digits. The host
 // propagates carries into ReproSum limbs and rounds with ReproSum::value.
 constexpr int kDigits = 70;
+// Per check iteration: 5 x 70 digit words, then the 5 L-inf maxima (bits of
+// max |R_v|), padded (CAV_NORM_WORDS in cavity_b200.h).
+constexpr int kNormWords = CAV_NORM_WORDS;
+static_assert(kNormWords >= 5 * kDigits + 5, "norm words");
 
 struct TermPieces {
   int d;            // first digit

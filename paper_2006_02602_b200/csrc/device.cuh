@@ -11,15 +11,16 @@
 namespace cav {
 
 // Per-iteration scalars every kernel of iteration n reads: the step dt_n and
-// the pending centre-pressure shift pc_{n-1} (0 when rescale is off or n==1).
-// Eager mode (single-rank TMA pipeline) stores the rescaled pressure
+// the centre-pressure shift pcs_n. Every block stores the rescaled pressure
 // directly: the updated p' of iteration n is written as fl(p' - pcs_n), where
 // pcs_n = p'(centre) is computed ahead of the step from the same inputs with
-// the same arithmetic (center_p_update). pc is then 0 (nothing pending).
+// the same arithmetic (center_p_update on one rank; k_fold over the gathered
+// centre stencil on many). That is exactly rescale_pressure
+// (src/solver.cpp:248-257), so stored states are always final.
 struct IterScalars {
   double dt;
-  double pc;   // lazy shift consumers apply on load (pending pc_{n-1})
-  double pcs;  // eager shift the step applies on store (pc_n), else 0
+  double pc;   // 0: no shift is ever pending (kept for the op-level k_bc signature)
+  double pcs;  // shift the step applies on store (pc_n; 0 with rescale off)
   double pad;
 };
 
@@ -27,8 +28,7 @@ struct IterScalars {
 struct Acc {
   unsigned long long dmax[3];  // bit patterns of max(|u|+beta), ... (all >= u_ref > 0)
   unsigned long long err;      // min error code, ~0 = none
-  double pc_local;             // p' at the centre node, on its owner
-  unsigned long long pad[3];
+  unsigned long long pad[4];
 };
 
 // Error code ordering = the reference's reporting order: earliest iteration,
@@ -42,6 +42,17 @@ __host__ __device__ __forceinline__ unsigned long long err_code(long long it, in
 }
 
 __device__ __forceinline__ double dmax_d(double a, double b) { return a < b ? b : a; }
+
+// |x| as bits: for non-negative doubles (and +inf, then NaN) the unsigned
+// order of the bit patterns is the numeric order, so an integer max is the
+// exact L-inf maximum (any grouping, any order).
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
 
 // Loads one cell's star from global memory (layout g). Pressure values of
 // interior cells get the pending rescale shift fl(p - pc); ghost values are

@@ -2,11 +2,19 @@
 // block ABI (/root/reference/proj/src/runner.cpp:259-396). Like the
 // reference, one host thread per rank; each thread owns one block on its GPU
 // (cfg.devices[rank % 8]). Cross-rank traffic never touches the host: halos
-// and scalars move GPU-to-GPU inside the iteration kernels. The host only
-// joins at convergence checks (to fold exact norm partials, as global_norms
-// does at src/runner.cpp:81-104) and at the end.
+// and scalars move GPU-to-GPU (peer stores, stream-ordered waits). The host
+// only joins at convergence checks (to fold exact norm partials, as
+// global_norms does at src/runner.cpp:81-104) and at the end.
+//
+// cfg.seed != 0 is the GPU analogue of the reference's randomized bus
+// (src/inproc.cpp:92-114, acceptance c8): rank threads start in a seeded
+// shuffled order and each block pauses at seeded random points between
+// iterations, so ranks run at skewed times; results must not change.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <numeric>
+#include <random>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -84,7 +92,7 @@ struct Shared {
   std::vector<std::exception_ptr> errors;
   std::vector<double> seconds;
   std::vector<cav_ledger> ledgers;
-  std::vector<std::vector<uint64_t>> digits;  // per rank, current segment
+  std::vector<std::vector<uint64_t>> digits;  // per rank, current segment (CAV_NORM_WORDS per check)
   std::vector<long long> check_iters;
   // rank 0 owned results
   long long marched = 0;
@@ -92,6 +100,7 @@ struct Shared {
   bool stop = false;
   std::vector<long long> hist_it;
   std::vector<std::array<double, 5>> hist;
+  std::vector<std::array<double, 5>> hist_linf;
   std::array<double, 5> peaks{};
   double* fields = nullptr;
 
@@ -107,18 +116,24 @@ void fold_norms(Shared& sh, long long n_checks) {
   const bool fixed = sh.cfg->steps >= 0;
   for (long long c = 0; c < n_checks; ++c) {
     std::array<double, 5> l2{};
+    std::array<double, 5> linf{};
     for (int v = 0; v < 5; ++v) {
       uint64_t total[70] = {};
+      uint64_t mx = 0;
       for (int r = 0; r < sh.np; ++r) {
+        const uint64_t* w = sh.digits[r].data() + c * CAV_NORM_WORDS;
         uint64_t limbs[70];
-        host::digits_to_limbs(sh.digits[r].data() + (c * 5 + v) * 70, limbs);
+        host::digits_to_limbs(w + v * 70, limbs);
         host::repro_merge(total, limbs);
+        mx = std::max(mx, w[5 * 70 + v]);  // L-inf: exact max of |R| bit patterns
       }
       l2[v] = std::sqrt(host::repro_value(total) / static_cast<double>(nglobal));
+      std::memcpy(&linf[v], &mx, sizeof mx);
     }
     const long long it = sh.check_iters[c];
     sh.hist_it.push_back(it);
     sh.hist.push_back(l2);
+    sh.hist_linf.push_back(linf);
     if (sh.cfg->monitor_every > 0 && it % sh.cfg->monitor_every == 0)
       std::printf("iter %8lld  |R|: p=%.3e u=%.3e v=%.3e w=%.3e T=%.3e\n", it, l2[0], l2[1], l2[2], l2[3], l2[4]);
     if (!fixed) {
@@ -149,6 +164,7 @@ void rank_main(Shared& sh, int rank) {
   d.corrupt_exchange = sh.opt->corrupt_exchange;
   d.device = cfg.devices[rank % 8];
   d.timeout_ms = cfg.timeout_ms > 0 ? cfg.timeout_ms : 20000.0;
+  d.jitter_seed = cfg.seed;
   cav_block* b = nullptr;
   check(cav_block_create(&d, &b));
   sh.blocks[rank] = b;
@@ -184,7 +200,7 @@ void rank_main(Shared& sh, int rank) {
     long long nchk = 0;
     for (long long q = it; q <= end; ++q) nchk += norms && (q == 1 || q % cadence == 0);
     std::vector<uint64_t>& dig = sh.digits[rank];
-    dig.assign(static_cast<size_t>(std::max<long long>(1, nchk)) * 350, 0);
+    dig.assign(static_cast<size_t>(std::max<long long>(1, nchk)) * CAV_NORM_WORDS, 0);
     std::vector<long long> citers(static_cast<size_t>(std::max<long long>(1, nchk)));
     io.first_it = it;
     io.n_its = nits;
@@ -244,10 +260,11 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
     if (cfg->np < 1 || cfg->np > 512) throw std::invalid_argument("run: np must be in 1..512");
     const auto dims = host::decomp_dims(cfg->np, cfg->mode, cfg->dims);
     host::cavity_spacing(cfg->nx, cfg->ny, cfg->nz, cfg->fluid.length, cfg->fluid.length, cfg->fluid.length);
-    // Ranks sharing a GPU each drive 2 streams whose spinning kernels wait on
-    // each other; CUDA multiplexes streams onto CUDA_DEVICE_MAX_CONNECTIONS
-    // hardware queues (default 8), and two streams on one queue would
-    // serialise a waiter ahead of the kernel it waits for.
+    // Ranks sharing a GPU each drive 3 streams, two of which wait (stream
+    // memory operations) for work of other ranks; CUDA multiplexes streams
+    // onto CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8), and two
+    // streams on one queue would serialise a waiter ahead of the work it
+    // waits for.
     {
       int per_dev[8] = {};
       for (int r = 0; r < cfg->np; ++r) ++per_dev[cfg->devices[r % 8] & 7];
@@ -255,9 +272,9 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
       for (int d = 0; d < 8; ++d) most = std::max(most, per_dev[d]);
       const char* env = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
       const int conns = env ? std::atoi(env) : 8;
-      if (most > 1 && 2 * most > conns)
+      if (most > 1 && 3 * most > conns)
         throw std::invalid_argument("run: " + std::to_string(most) + " ranks share one GPU; set CUDA_DEVICE_MAX_CONNECTIONS >= " +
-                                    std::to_string(2 * most) + " (max 32) before CUDA initialises");
+                                    std::to_string(3 * most) + " (max 32) before CUDA initialises");
     }
     Shared sh(cfg, opt, cfg->np);
     sh.gn = {cfg->nx, cfg->ny, cfg->nz};
@@ -273,7 +290,12 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
       }
     } else {
       std::vector<std::thread> threads;
-      for (int r = 0; r < sh.np; ++r)
+      std::vector<int> order(sh.np);
+      std::iota(order.begin(), order.end(), 0);
+      std::mt19937_64 rng(cfg->seed);
+      if (cfg->seed) std::shuffle(order.begin(), order.end(), rng);
+      for (int r : order) {
+        if (cfg->seed) std::this_thread::sleep_for(std::chrono::microseconds(rng() % 2000));
         threads.emplace_back([&sh, r] {
           try {
             rank_main(sh, r);
@@ -282,24 +304,19 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
             sh.bar.poison(r);
           }
         });
+      }
       for (auto& t : threads) t.join();
     }
-    if (std::getenv("CAV_DEBUG_DUMP")) {  // diagnostics: progress stamps of every rank
+    if (std::getenv("CAV_DEBUG_DUMP")) {  // diagnostics: receive flags and scalar stamps of every rank
       for (int r = 0; r < sh.np; ++r) {
         if (!sh.blocks[r]) continue;
-        std::vector<uint64_t> v(130 + 16 * sh.np + 7 + 6);
+        std::vector<uint64_t> v(64 + 2 * sh.np + 2);
         if (cav_block_debug(sh.blocks[r], v.data(), static_cast<int>(v.size())) != CAV_OK) continue;
         std::fprintf(stderr, "rank %d flags", r);
-        for (int q = 0; q < 6; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[q]);
+        for (int q = 0; q < 6; ++q) std::fprintf(stderr, " %llx", (unsigned long long)v[q]);
         std::fprintf(stderr, " | stamps");
-        for (int q = 0; q < 2 * sh.np; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[64 + 8 * q + 5]);
-        std::fprintf(stderr, " | progress");
-        for (int q = 0; q < 7; ++q) std::fprintf(stderr, " %llu", (unsigned long long)v[130 + 16 * sh.np + q]);
-        double hm[6];
-        std::memcpy(hm, v.data() + 137 + 16 * sh.np, sizeof hm);
-        std::fprintf(stderr, " | host ms: ready %.3f prologue %.3f it1 %.3f enq %.3f sync %.3f (t0 %.6f)\n",
-                     1e3 * (hm[1] - hm[0]), 1e3 * (hm[2] - hm[0]), 1e3 * (hm[3] - hm[0]), 1e3 * (hm[4] - hm[0]),
-                     1e3 * (hm[5] - hm[0]), hm[0]);
+        for (int q = 0; q < 2 * sh.np; ++q) std::fprintf(stderr, " %llx", (unsigned long long)v[64 + q]);
+        std::fprintf(stderr, "\n");
       }
     }
     for (auto* b : sh.blocks)
@@ -339,6 +356,8 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
     for (size_t n = 0; n < sh.hist.size() && static_cast<long long>(n) < out->hist_capacity; ++n) {
       out->hist_iter[n] = sh.hist_it[n];
       for (int v = 0; v < 5; ++v) out->hist_l2[5 * n + v] = sh.hist[n][v];
+      if (out->hist_linf)
+        for (int v = 0; v < 5; ++v) out->hist_linf[5 * n + v] = sh.hist_linf[n][v];
     }
   });
 }

@@ -13,10 +13,11 @@
 // wall ghosts of apply_boundary_conditions (src/solver.cpp:158-191) are formed
 // in registers by the warps whose cells touch a wall (the same
 // apply_wall_ghosts the pointwise kernels use), like the z-wall ghosts in the
-// k-window. Only a pending lazy rescale fl(p - pc) (multi-rank blocks) is
-// patched in place, by all consumer threads, then a consumer-only named
-// barrier. (Measured: a dedicated patcher warp, or cooperative smem wall
-// patches with a barrier per plane, cost 25% of the step on 256^3.)
+// k-window, or (G) already stored in the state. The ring is never patched:
+// every block stores its rescaled pressure eagerly (fl(p' - pcs_n), see
+// IterScalars), so landed tiles hold final values. (Measured: a dedicated
+// patcher warp, or cooperative smem patches with a barrier per plane, cost
+// 25% of the step on 256^3.)
 //
 // Each consumer keeps its column's p k-window in registers (k-2..k+3; z-wall
 // ghosts are formed there) and reads u,v,w,T at k-1..k+1 from the slots it
@@ -31,6 +32,14 @@
 // rows are L2 hits), slower items (wall tiles) do not unbalance the SMs, and
 // each item restarts the k-window once. The last items in the order are
 // short k-chunks, which shortens the tail where CTAs run out of work.
+//
+// Overlap (multi-rank blocks, src/runner.cpp:189-194): the item space is
+// split into internal items, whose stencils never reach a joined face's halo,
+// and shell items (the tile columns / rows and the 2-plane z chunks next to a
+// joined face). One launch takes the internal items while the halo exchange
+// is in flight, a second one the shell items after it landed; both are the
+// same TMA kernel, so the shells run at full speed (the reference's shells
+// of src/overlap.cpp:13-28 are a subset of these).
 #pragma once
 
 #include <cuda.h>
@@ -122,7 +131,7 @@ struct TmaCfg {
   static constexpr int TxBytes = (kPW * PH + 4 * QField) * 8;  // bytes the two boxes deliver
   static constexpr int Threads = 32 * (TY + 1);  // consumers + issuer
   static constexpr int NC = 32 * TY;              // consumer threads
-  static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + 5 * kDigits * 8;
+  static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + (5 * kDigits + 8) * 8;
   static_assert(PField * 8 % 128 == 0 && Slot * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
   static_assert(R >= 5, "ring must hold planes k..k+3 plus one in flight");
 };
@@ -133,8 +142,7 @@ struct TmaStepArgs {
   cav_stencil_params sp;
   BetaFast bf;  // beta shortcuts (host::beta_fast)
   unsigned* work;  // dynamic item counter (items >= gridDim.x), reset by the last CTA
-  int eager;      // store fl(p' - sc->pcs) and fold pcs_{n+1} (single rank); see IterScalars
-  const int* stop;  // device convergence: set once converged, later steps do nothing (or null)
+  const int* stop;  // set once converged (single rank) or aborted (timeout): later steps do nothing (or null)
   cav_box box;
   const IterScalars* sc;
   Acc* acc;
@@ -148,9 +156,16 @@ struct TmaStepArgs {
   // bigend: the items claimed last are short, which shortens the tail where
   // CTAs run out of work at different times
   int nbig, chunk_tail, bigend;
+  // z chunks: zl (0/1) two-plane shell chunks at box.lo[2] and zh at
+  // box.hi[2] (joined z faces), the rest from mlo = box.lo[2] + 2 zl as above
+  int zl, zh, mlo;
+  // item subset: 0 all, 1 internal only, 2 shell only; a tile is a shell
+  // tile unless sx0 <= tile_x < sx1 and sy0 <= tile_y < sy1 (tile columns /
+  // rows holding the two cell layers next to a joined face)
+  int part, sx0, sx1, sy0, sy1;
   WallInfo walls;
-  // single-rank fold (replaces k_scalar_sync when np == 1): the last CTA to
-  // finish turns this iteration's maxima into dt_{n+1} and publishes pc_n
+  // single-rank fold (np == 1; many ranks fold in k_fold): the last CTA to
+  // finish turns this iteration's maxima into dt_{n+1} and pcs_{n+1}
   int fold;
   unsigned* done;
   IterScalars* sc_next;
@@ -180,14 +195,32 @@ __device__ __forceinline__ ItemGeom item_geom(const TmaStepArgs& a, long long it
   ItemGeom r;
   r.ti0 = a.box.lo[0] + (tile % a.tiles_x) * 32;
   r.tj0 = a.box.lo[1] + (tile / a.tiles_x) * TY;
-  if (chunk < a.nbig) {
-    r.kb = a.box.lo[2] + chunk * a.chunk;
+  const int m = chunk - a.zl;
+  if (m < 0) {
+    r.kb = a.box.lo[2];
+    r.ke = r.kb + 2;
+  } else if (chunk >= a.nchunks - a.zh) {
+    r.ke = a.box.hi[2];
+    r.kb = r.ke - 2;
+  } else if (m < a.nbig) {
+    r.kb = a.mlo + m * a.chunk;
     r.ke = min(r.kb + a.chunk, a.bigend);
   } else {
-    r.kb = a.bigend + (chunk - a.nbig) * a.chunk_tail;
-    r.ke = min(r.kb + a.chunk_tail, a.box.hi[2]);
+    r.kb = a.bigend + (m - a.nbig) * a.chunk_tail;
+    r.ke = min(r.kb + a.chunk_tail, a.box.hi[2] - 2 * a.zh);
   }
   return r;
+}
+
+// Whether `item` belongs to this launch's subset (TmaStepArgs::part).
+__device__ __forceinline__ bool item_wanted(const TmaStepArgs& a, long long item) {
+  if (a.part == 0) return true;
+  const int chunk = static_cast<int>(item / a.ntiles);
+  const int tile = static_cast<int>(item % a.ntiles);
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const bool shell = chunk < a.zl || chunk >= a.nchunks - a.zh || tx < a.sx0 || tx >= a.sx1 || ty < a.sy0 ||
+                     ty >= a.sy1;
+  return shell == (a.part == 2);
 }
 
 // Consumer-side star accessor: p's in-plane neighbours from the landed slot
@@ -272,35 +305,6 @@ struct SmemAcc {
   __device__ __forceinline__ double tzp() const { return on(kZhi1) ? t() : Up[3 * QF]; }
 };
 
-// In-place lazy rescale fl(p - pc) of the interior pressure of a landed plane
-// tile (rescale_pressure, src/solver.cpp:248-257) by all NC consumer threads
-// (t = consumer thread index).
-template <class Cfg>
-__device__ __forceinline__ void coop_rescale(double* P, const TmaStepArgs& a, const ItemGeom& it, double pc, int t) {
-  constexpr int PAIRS = kPW / 2, N = Cfg::PH * PAIRS;
-  const Geo& g = a.g;
-  const int i0 = it.ti0 - 2, j0 = it.tj0 - 2;
-  for (int idx = t; idx < N; idx += Cfg::NC) {
-    const int row = idx / PAIRS, c = idx - row * PAIRS;
-    const int j = j0 + row, i = i0 + 2 * c;
-    if (j >= 2 && j < g.ny + 2) {
-      double2* q = reinterpret_cast<double2*>(P + row * kPW + 2 * c);
-      double2 v = *q;
-      if (i >= 2 && i < g.nx + 2) v.x = v.x - pc;
-      if (i + 1 >= 2 && i + 1 < g.nx + 2) v.y = v.y - pc;
-      *q = v;
-    }
-  }
-}
-
-// Whether plane `pl` of item `it` needs the lazy rescale before use: a shift
-// is pending (multi-rank blocks) and its bit pattern is not +0.0 (subtracting
-// +0.0 is the identity; subtracting -0.0 is not). Uniform across the CTA's
-// consumer warps, so the named barrier it implies is too.
-__device__ __forceinline__ bool plane_needs_rescale(const TmaStepArgs& a, int pl, bool lazy) {
-  return lazy && pl >= 2 && pl < a.g.nz + 2;  // ghost planes are read only as column values
-}
-
 // TMA issue cursor of the issuer warp (lane 0). (Measured: folding it into
 // consumer warp 0 to free a warp slot was 16% slower — the ring is only fed
 // when that warp reaches a wait.) Items:
@@ -337,7 +341,9 @@ __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, cons
     tma::load_4d(dst, mP, x0, y0, q.pl, 0, &full[q.s]);
     tma::load_4d(dst + Cfg::PField, mQ, x0, y0 + 1, q.pl, 0, &full[q.s]);
     if (++q.pl > q.it.ke + 1) {
-      q.item = gridDim.x + atomicAdd(a.work, 1u);
+      do {
+        q.item = gridDim.x + atomicAdd(a.work, 1u);
+      } while (q.item < total && !item_wanted(a, q.item));
       if (q.item >= total) {
         q.done = true;
       } else {
@@ -358,8 +364,10 @@ __device__ __forceinline__ bool issue_one(Issuer& q, const CUtensorMap* mP, cons
 // shifted mantissas (m << (off & 31), < 2^85) are summed in 96 bits and
 // flushed to the CTA's carry-save digit words when a term starts at a
 // different digit (neighbouring cells of a column mostly share a binade), at
-// the end of each item (at most 48 terms per run, so 96 bits cannot
-// overflow) and at the end. The digit words are carry-save, so any grouping
+// the end of each item and at the end. Each shifted mantissa is below 2^84,
+// so 96 bits hold 2^12 = 4096 terms: the step's runs are bounded by one
+// item's k-chunk (checked on the host), k_norm_runs' by its segment
+// (kNormRunSeg, static_assert there). The digit words are carry-save, so any grouping
 // gives the same words as ReproSum::add term by term (measured: a 256^3 check
 // iteration 1.7 -> 1.4 ms against warp-aggregated atomics per term; 96 rather
 // than 128 bits frees 5 registers).
@@ -427,18 +435,17 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (NORMS)
-    for (int x = threadIdx.x; x < 5 * kDigits; x += kTmaThreads) sdig[x] = 0;
+    for (int x = threadIdx.x; x < 5 * kDigits + 5; x += kTmaThreads) sdig[x] = 0;  // digits, then 5 L-inf maxima
   __syncthreads();
 
   const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
-  const double pc = a.sc->pc;
-  const bool lazy = __double_as_longlong(pc) != 0;
 
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
     if (lane != 0) return;
     Issuer iq{};
     iq.item = blockIdx.x;
+    while (iq.item < total && !item_wanted(a, iq.item)) iq.item = gridDim.x + atomicAdd(a.work, 1u);
     iq.done = iq.item >= total;
     if (!iq.done) {
       iq.it = item_geom<C>(a, iq.item);
@@ -462,6 +469,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   unsigned e_p = 0, e_u = 0, e_v = 0, e_w = 0, e_t = 0;  // max exponent field per variable
   unsigned nbad = 0;
   DigitRun runs[NORMS && !G ? 5 : 1];
+  unsigned long long lmax[NORMS && !G ? 5 : 1] = {};  // L-inf: bits of max |R_v|
   const long long rdelta = NORMS && G ? a.rs - a.out : 0;
   for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
   const double* ringc = ring + (ty + 2) * kPW + tx + 2;                 // own p cell in slot 0
@@ -475,31 +483,19 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       ph ^= 1;
     }
   };
-  // Wait for the next 1 or 2 entries to land. With a pending lazy shift
-  // (multi-rank blocks) all consumer threads rescale the landed p tile in
-  // place, a named barrier makes that visible to every consumer warp, and the
-  // writers' proxy fence orders it before the slot's next TMA fill.
-  const int tid = threadIdx.x;
+  // Wait for the next 1 or 2 entries to land.
   int wfl = 0;         // wall flags of this thread's column (kXlo2 ... kYhi0)
   bool wx = false, wyz = false;  // some lane of this warp has an x / y wall flag (warp-uniform)
   // G: this lane's column lies inside the box. Lanes outside it (ragged
   // tiles) compute on whatever the slot holds there, without storing or reducing, so
   // the cell is not under a branch (1.4% faster at 256^3).
   bool live = true;
-  auto wait_planes = [&](const ItemGeom& it, int pl, int count, int* sl) {
-    bool any = false;
+  auto wait_planes = [&](int count, int* sl) {
     for (int q = 0; q < count; ++q) {
       sl[q] = sw;
       tma::mbar_wait_s(full_s + 8u * sw, phw);
       advance(sw, phw);
-      any = any || (!G && plane_needs_rescale(a, pl + q, lazy));  // G: eager, never a pending shift
     }
-    if (any) {
-      for (int q = 0; q < count; ++q)
-        if (plane_needs_rescale(a, pl + q, lazy)) coop_rescale<Cfg>(ring + sl[q] * kTmaSlot, a, it, pc, tid);
-      tma::named_sync(1, Cfg::NC);
-    }
-    if (any) tma::fence_proxy_async();
   };
   auto release_slot = [&](int sl) {
     __syncwarp();
@@ -544,7 +540,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // one cell at plane kk: residual + update + store + bookkeeping. Slots
   // slm, slk, slp hold planes kk-1, kk, kk+1.
   auto cell = [&](int slm, int slk, int slp, int kk, double p0, double pzm, double pzp, double pzm2, double pzp2,
-                  double* op, bool ccolk) {
+                  double* op) {
     const int zf = G ? 0 : (zlo && kk == 2 ? kZlo2 : 0) | (zhi && kk == g.nz + 1 ? kZhi1 : 0);
     Res r;
     double uc, vc, wc, tc;
@@ -602,8 +598,6 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       e_w = max(e_w, static_cast<unsigned>(__double2hiint(qwn)) & 0x7FF00000u);
       e_t = max(e_t, static_cast<unsigned>(__double2hiint(qtn)) & 0x7FF00000u);
     }
-    // pc_n for the lazy shift (eager blocks fold pcs with center_p_update)
-    if (!G && ccolk) a.acc->pc_local = qpp;
     if (NORMS && G && live) {
       double* rp = op + rdelta;
       __stcs(rp, r.p);
@@ -613,11 +607,13 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       __stcs(rp + 4 * fs, r.t);
     }
     if (NORMS && !G) {
-      const double rr[5] = {r.p * r.p, r.u * r.u, r.v * r.v, r.w * r.w, r.t * r.t};
+      const double rv[5] = {r.p, r.u, r.v, r.w, r.t};
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
-        if (nonfinite(rr[v])) nbad = 1;
-        else digit_run_add(runs[v], sdig + v * kDigits, rr[v]);
+        lmax[v] = max(lmax[v], abs_bits(rv[v]));
+        const double rr = rv[v] * rv[v];
+        if (nonfinite(rr)) nbad = 1;
+        else digit_run_add(runs[v], sdig + v * kDigits, rr);
       }
     }
   };
@@ -630,7 +626,6 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const int len = it.ke - it.kb;
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
-    const bool ccol = i == a.cx && j == a.cy;
     live = active;
     // x/y walls next to this thread's column: register ghosts (SmemAcc<.., true>)
     if (G && a.gw) {  // wfl (G): 1 = i == 2 at the low x wall, 2 = i == nx+1 at the high one, 4 = in this warp
@@ -651,8 +646,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     // prologue: planes kb-2 .. kb+1; p window from all four, the slots of
     // kb-1 .. kb+1 stay held for u,v,w,T
     int sa[2], sb[2];
-    wait_planes(it, it.kb - 2, 2, sa);
-    wait_planes(it, it.kb, 2, sb);
+    wait_planes(2, sa);
+    wait_planes(2, sb);
     double P[6];  // p at planes k-2 .. k+3
     P[0] = slot(sa[0])[0];
     P[1] = slot(sa[1])[0];
@@ -669,14 +664,14 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       // of extra time to land. The z-wall rules read P[0..4] only; a ghost
       // P[5] they form (k+3 >= nz+2) is not overwritten by the slot.
       int sn[2];
-      wait_planes(it, k + 2, 1, sn);
+      wait_planes(1, sn);
       P[4] = slot(sn[0])[0];
       const bool zh5 = !G && zhi && k + 3 >= g.nz + 2;
       if (!G && ((zlo && k <= 3) || zh5)) zwall2(P, k);
-      if (G || active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
-      wait_planes(it, k + 3, 1, sn + 1);
+      if (G || active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op);
+      wait_planes(1, sn + 1);
       if (!zh5) P[5] = slot(sn[1])[0];
-      if (G || active) cell(sk0, sk1, sn[0], k + 1, P[3], P[2], P[4], P[1], P[5], op + plane, ccol && k + 1 == a.cz);
+      if (G || active) cell(sk0, sk1, sn[0], k + 1, P[3], P[2], P[4], P[1], P[5], op + plane);
       release_slot(skm);
       release_slot(sk0);
       skm = sk1;
@@ -690,10 +685,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     if (st < len) {  // odd remainder: one plane
       const int k = it.kb + st;
       int sn[2];
-      wait_planes(it, k + 2, 1, sn);  // plane k+2
+      wait_planes(1, sn);  // plane k+2
       P[4] = slot(sn[0])[0];
       if (!G && ((zlo && k <= 3) || (zhi && k + 2 >= g.nz + 2))) zwall1(P, k);
-      if (G || active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op, ccol && k == a.cz);
+      if (G || active) cell(skm, sk0, sk1, k, P[2], P[1], P[3], P[0], P[4], op);
       release_slot(sn[0]);
     }
     // planes ke-1 .. ke+1 (odd: plus ke+2 above) served only as neighbours
@@ -710,7 +705,11 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
 
   if (NORMS && !G)
 #pragma unroll
-    for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sdig + v * kDigits);
+    for (int v = 0; v < 5; ++v) {
+      digit_run_flush(runs[v], sdig + v * kDigits);
+      const unsigned long long m = warp_max_u64(lmax[v]);
+      if (lane == 0 && m) atomicMax(&sdig[5 * kDigits + v], m);
+    }
   // consumer-only reductions
   constexpr int NC = 32 * C;
   __shared__ double sred[3][C];
@@ -751,16 +750,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         fl.alpha = a.alpha;
         const double dtn = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, fl, a.cfl);
         a.sc_next->dt = dtn;
-        if (a.eager) {
-          // this iteration's output is final; pcs_{n+1} = p'(centre) of the
-          // next step, from the same inputs and arithmetic as that step
-          a.sc_next->pc = 0.0;
-          a.sc_next->pcs = a.rescale ? center_p_update(a.out, a.g, a.walls, a.sp, a.bf, dtn, 0.0, a.cx,
-                                                       a.cy, a.cz)
-                                     : 0.0;
-        } else {
-          a.sc_next->pc = a.rescale ? acc->pc_local : 0.0;
-        }
+        // this iteration's output is final; pcs_{n+1} = p'(centre) of the
+        // next step, from the same inputs and arithmetic as that step
+        a.sc_next->pcs = a.rescale ? center_p_update(a.out, a.g, a.walls, a.sp, a.bf, dtn, 0.0, a.cx, a.cy, a.cz)
+                                   : 0.0;
         const unsigned long long e = acc->err;
         if (e < *a.err_sticky) *a.err_sticky = e;
         Acc z{};
@@ -770,9 +763,12 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       *a.done = 0;
     }
   }
-  if (NORMS && !G)
+  if (NORMS && !G) {
     for (int x = threadIdx.x; x < 5 * kDigits; x += NC)
       if (sdig[x]) atomicAdd(&a.digits[x], sdig[x]);
+    if (threadIdx.x < 5 && sdig[5 * kDigits + threadIdx.x])
+      atomicMax(&a.digits[5 * kDigits + threadIdx.x], sdig[5 * kDigits + threadIdx.x]);
+  }
 }
 
 }  // namespace cav

@@ -1,10 +1,11 @@
 # GPU parity suite + smoke (+ optional bench), results in gpurun_out/
+# usage: gpu_tests.sh [TAG] [pytest -k expression]
 cd $GRAFT_REPO_ROOT
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+export PYTHONUNBUFFERED=1
+TAG=${1:-t}
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 echo "smoke exit $?"
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+if [ -n "$2" ]; then K="-k $2"; else K=""; fi
+timeout 2400 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider $K --durations=15 > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo "pytest exit $?"
-if [ "$1" = "bench" ]; then
-  timeout 300 python bench.py --steps 2000 --warmup 20 --cpu-seconds 10 > gpurun_out/bench.log 2>&1
-  echo "bench exit $?"
-fi
+tail -5 gpurun_out/pytest_gpu_$TAG.log

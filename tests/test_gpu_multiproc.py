@@ -50,7 +50,7 @@ def _worker(rank, world, port, grid, dims, strategy, overlap, steps, q):
         lo = b.lo
         n = b.n
         interior = store[:, 2:n[2] + 2, 2:n[1] + 2, 2:n[0] + 2].copy()
-        q.put((rank, "ok", lo, interior, [(it, d.copy()) for it, d in checks]))
+        q.put((rank, "ok", lo, interior, [(it, d.copy()) for it, d, _ in checks]))
         dist.barrier()
         b.close()
     except Exception as ex:

@@ -1,0 +1,142 @@
+"""Robustness parity on the GPU path and the L-inf residual
+norm north_star asks for:
+
+* a peer that never runs raises TransportTimeout naming the waiting rank and
+  every stuck (source, tag) pair, as InprocTransport::wait_all does
+  (/root/reference/proj/src/inproc.cpp:145-177, pinned by
+  tests/test_transport.cpp:114-133) — the waits are stream-ordered, so the
+  timeout is raised by the host, and the block's streams drain afterwards;
+* seeded randomized rank timing (the GPU analogue of the reference's shuffled
+  delivery, src/inproc.cpp:92-114 / acceptance c8, tests/acceptance.cpp:
+  591-628): two 8-rank overlapped runs with skewed rank start times and
+  random pauses give byte-identical fields, norms and ledgers, equal to the
+  unperturbed run;
+* L-inf norms max |R_v| per check iteration equal numpy's max over the
+  oracle's residual fields (the reference has only L2; src/solver.cpp:259-285
+  defines which residual a check iteration reduces);
+* a device-converged solve on the stored-ghost path stops where the oracle
+  does, with one exchange per marched iteration in the ledger.
+"""
+import numpy as np
+import pytest
+
+import oracle_ops as O
+from oracle.refbind import Oracle
+from paper_2006_02602_b200 import capi
+from paper_2006_02602_b200.capi import TransportTimeout
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def test_timeout_names_waiting_rank_and_stuck_sources():
+    grid, dims = (30, 12, 10), (3, 1, 1)
+    blocks = [capi.Block(r, 3, grid, dims, strategy="v3", timeout_ms=300.0) for r in range(3)]
+    for b in blocks:
+        for r in range(3):
+            if r != b.desc.rank:
+                b.connect(r, ptr=blocks[r].arena())
+        b.initialize()
+    # ranks 1 and 2 never march: rank 0 waits for their scalars and rank 1's halo
+    with pytest.raises(TransportTimeout) as ex:
+        blocks[0].run(3)
+    msg = str(ex.value)
+    assert msg.startswith("rank 0: receive timed out")
+    assert "(src=1, tag=1001)" in msg and "(src=2, tag=1001)" in msg
+    entry = [e for e in capi.build_plan(blocks[0].n, capi.neighbors(dims, 0), "v3")][0]
+    assert f"(src=1, tag={entry['recv_tag']})" in msg
+    # the aborted block refuses further work and still closes (its streams drained)
+    with pytest.raises(capi.LogicError):
+        blocks[0].run(1)
+    for b in blocks:
+        b.close()
+
+
+def test_timeout_at_a_later_iteration():
+    """A peer that stops after some iterations: the waiting rank names it at
+    the first iteration it cannot complete."""
+    grid, dims = (20, 12, 10), (2, 1, 1)
+    a, b = (capi.Block(r, 2, grid, dims, strategy="v3", overlap=True, timeout_ms=300.0) for r in range(2))
+    a.connect(1, ptr=b.arena())
+    b.connect(0, ptr=a.arena())
+    a.initialize()
+    b.initialize()
+    import threading
+    t = threading.Thread(target=lambda: b.run(4))
+    t.start()
+    with pytest.raises(TransportTimeout) as ex:
+        a.run(10)
+    t.join()
+    # rank 1 marched iterations 1..4: its scalars reach rank 0's fold of
+    # iteration 5, its halo of iteration 5 never comes
+    entry = capi.build_plan(a.n, capi.neighbors(dims, 0), "v3")[0]
+    assert str(ex.value).startswith("rank 0: receive timed out at iteration 5; outstanding: ")
+    assert f"(src=1, tag={entry['recv_tag']})" in str(ex.value)
+    a.close()
+    b.close()
+
+
+def test_seeded_rank_timing_is_deterministic():
+    base = dict(grid=(24, 24, 24), steps=60, np=8, strategy="v3", overlap=1, check_every=10)
+    plain = capi.run_case(capi.default_config(**base), collect_fields=True, collect_history=True)
+    runs = [capi.run_case(capi.default_config(seed=s, **base), collect_fields=True, collect_history=True)
+            for s in (20260131, 20260131, 7)]
+    for r in runs:
+        np.testing.assert_array_equal(bits(r.fields), bits(plain.fields))
+        np.testing.assert_array_equal(bits(r.history), bits(plain.history))
+        assert r.ledgers == plain.ledgers
+    want = Oracle.run_case(capi.default_config(grid=(24, 24, 24), steps=60, check_every=10), collect_fields=True,
+                           collect_history=True)
+    np.testing.assert_array_equal(bits(plain.fields), bits(want["fields"]))
+
+
+def _oracle_linf(n, steps, check_every, fluid, cfl=0.4):
+    """max |R_v| over the interior at every check iteration of the oracle's
+    serial loop (BC, residual, dt, update, rescale) from the quiescent state."""
+    f = np.zeros((5, n[2] + 4, n[1] + 4, n[0] + 4))
+    f[4] = fluid.t_inf
+    h = capi.cavity_spacing(n)
+    sp = O.stencil(h, fluid)
+    box = ((2, 2, 2), (n[0] + 2, n[1] + 2, n[2] + 2))
+    center = tuple((x - 1) // 2 + 2 for x in n)
+    out = []
+    for it in range(1, steps + 1):
+        f = O.bc(f, n, (1,) * 6, fluid)
+        r = O.residual(f, n, box, sp)
+        if it == 1 or it % check_every == 0:
+            inner = r[:, 2:n[2] + 2, 2:n[1] + 2, 2:n[0] + 2]
+            out.append(np.abs(inner).reshape(5, -1).max(axis=1))
+        dt = O.compute_dt(f, n, h, fluid, cfl)
+        for v in range(5):
+            f[v] = O.update(f[v], r[v], dt, n, box)
+        f[0] = O.rescale(f[0], n, f[0][center[2], center[1], center[0]])
+    return np.array(out)
+
+
+@pytest.mark.parametrize("kw, env", [(dict(), {}), (dict(), {"CAV_STORED_GHOSTS": "1"}),
+                                     (dict(np=2, mode="1d-i", strategy="v3", overlap=1), {}),
+                                     (dict(np=4, mode="2d", strategy="v3", overlap=1), {"CAV_STORED_GHOSTS": "1"})])
+def test_linf_norm_matches_numpy_over_oracle_residuals(monkeypatch, kw, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n = (24, 20, 16)
+    cfg = capi.default_config(grid=n, steps=40, check_every=5, u_ref=1e-3, **kw)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True)
+    want = _oracle_linf(n, 40, 5, cfg.fluid)
+    assert r.history_linf.shape == want.shape
+    np.testing.assert_array_equal(bits(r.history_linf), bits(want))
+    assert np.all(want[1:] > 0)
+
+
+def test_device_converged_solve_stored_ghosts(monkeypatch):
+    monkeypatch.setenv("CAV_STORED_GHOSTS", "1")
+    cfg = capi.default_config(grid=(20, 16, 12), steps=-1, conv_tol=1e-3)
+    r = capi.run_case(cfg, collect_fields=True, collect_history=True)
+    o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
+    assert r.converged and o["converged"] and r.steps_marched == o["steps_marched"]
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+    assert r.ledgers[0]["exchanges"] == r.steps_marched  # no ledger entries for the no-op tail
