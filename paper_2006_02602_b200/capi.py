@@ -94,7 +94,7 @@ def lib(fmad=False):
                                                  C.POINTER(C.c_uint64), _P]
         L.cav_copy_box_to.argtypes = [_P, _I, _I, C.POINTER(A.Box), _P, _P]
         L.cav_copy_box_from.argtypes = [_P, _I, _I, C.POINTER(A.Box), _P, _P]
-        L.cav_block_bench.argtypes = [_P, _LL, C.POINTER(_D), C.POINTER(_D)]
+        L.cav_block_bench.argtypes = [_P, _LL, C.POINTER(_D)]
         _libs[fmad] = L
     return _libs[fmad]
 

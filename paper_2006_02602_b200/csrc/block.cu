@@ -22,7 +22,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -423,17 +426,23 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
   const int i = b.lo[0] + static_cast<int>(col % bw), j = b.lo[1] + static_cast<int>((col / bw) % bh);
   const int k0 = b.lo[2] + static_cast<int>(col / (static_cast<long long>(bw) * bh)) * kNormRunSeg;
   unsigned nf = 0;
+  unsigned long long mx[5] = {0, 0, 0, 0, 0};
   if (col < static_cast<long long>(bw) * bh * ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg)) {
     DigitRun runs[5];
-    unsigned long long mx[5] = {0, 0, 0, 0, 0};
     for (auto& r : runs) r = DigitRun{-1, 0u, 0u, 0u};
     const long long fs = g.fstride, plane = static_cast<long long>(g.pitch) * g.ypitch;
     const int k1 = min(k0 + kNormRunSeg, b.hi[2]);
     const double* q = rs + g.idx(i, j, k0);
-    for (int k = k0; k < k1; ++k, q += plane) {
-      double x[5];
+    // two planes in flight ahead of the two being summed (the loads do not
+    // depend on the digit-run arithmetic; without the explicit lookahead the
+    // kernel was latency-bound at ~1.9 TB/s)
+    auto load = [&](double* x, int k) {
+      if (k < k1) {
 #pragma unroll
-      for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + v * fs);
+        for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + (k - k0) * plane + v * fs);
+      }
+    };
+    auto add = [&](const double* x) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         mx[v] = max(mx[v], abs_bits(x[v]));
@@ -441,13 +450,30 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
         if (nonfinite(x2)) nf = 1;
         else digit_run_add(runs[v], sd + v * kDigits, x2);
       }
+    };
+    double a0[5], a1[5], b0[5], b1[5];
+    load(a0, k0);
+    load(a1, k0 + 1);
+    for (int k = k0; k < k1; k += 2) {
+      load(b0, k + 2);
+      load(b1, k + 3);
+      add(a0);
+      if (k + 1 < k1) add(a1);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) {
+        a0[v] = b0[v];
+        a1[v] = b1[v];
+      }
     }
 #pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      digit_run_flush(runs[v], sd + v * kDigits);
-      mx[v] = warp_max_u64(mx[v]);
-      if ((threadIdx.x & 31) == 0 && mx[v]) atomicMax(&smx[v], mx[v]);
-    }
+    for (int v = 0; v < 5; ++v) digit_run_flush(runs[v], sd + v * kDigits);
+  }
+  // warp collectives with every lane present (the last block's tail lanes
+  // have no column: a full-mask shuffle inside the branch would wait forever)
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    mx[v] = warp_max_u64(mx[v]);
+    if ((threadIdx.x & 31) == 0 && mx[v]) atomicMax(&smx[v], mx[v]);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < 5 * kDigits; x += kNormRunThreads)
@@ -550,6 +576,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // `p` = field 0 with a 36 x (TY+4) box, `q` = fields 1..4 (u, v, w, T) with a
 // 34 x (TY+2) x 1 x 4 box (one TMA per plane for all four).
 CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw, int bh) {
+  // L2 sector promotion of the TMA reads (CAV_L2_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B)
+  static const int promo = getenv_int("CAV_L2_PROMO", 3);
+  static const CUtensorMapL2promotion kPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   CUtensorMap m;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.pitch), static_cast<cuuint64_t>(g.ypitch),
                               static_cast<cuuint64_t>(g.nz + 4), static_cast<cuuint64_t>(nfields)};
@@ -561,7 +592,7 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE, kPromo[promo & 3],
                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return m;
@@ -645,6 +676,27 @@ void stream_wait_geq(cudaStream_t st, const std::vector<std::pair<const unsigned
 // counters[] words
 constexpr int kCtrAbort = 60, kCtrWork = 62, kCtrDone = 63;
 
+// Host-side enqueue progress of a block, shared with the blocks of the same
+// process that connect to it (in-process ranks: cav_run_case's threads, or
+// several capi.Block objects). A stream wait is only enqueued after every
+// launch that produces its value has been enqueued: CUDA multiplexes streams
+// onto a fixed set of hardware queues, and a wait that sits in a queue ahead
+// of the work it waits for (another rank's stream mapped to the same queue)
+// would never be satisfied. With producers always enqueued first, every wait
+// finds its producer ahead of it in any queue they share, so the FIFO order
+// cannot deadlock. Peers in other processes (other contexts) need no such
+// ordering. Values carry the run generation like the device flags.
+struct HostProgress {
+  std::atomic<unsigned long long> push{0};  // base | it: push(it) enqueued (push(0) = +0 after prologue)
+  std::atomic<unsigned long long> pack{0};  // base | it: pack(it) enqueued
+};
+
+std::mutex g_reg_mu;
+std::map<const void*, std::shared_ptr<HostProgress>>& registry() {
+  static std::map<const void*, std::shared_ptr<HostProgress>> m;
+  return m;
+}
+
 struct Block {
   cav_block_desc d{};
   std::array<int, 3> gn{}, dims{}, n{};
@@ -666,6 +718,8 @@ struct Block {
   unsigned char* arena = nullptr;
   std::vector<unsigned char*> peer_arena;
   std::vector<bool> peer_ipc;
+  std::shared_ptr<HostProgress> prog = std::make_shared<HostProgress>();
+  std::vector<std::shared_ptr<HostProgress>> host_peer;  // in-process peers (else null)
   // device bookkeeping
   Acc* acc = nullptr;            // [2]
   IterScalars* sc = nullptr;     // [2]
@@ -731,7 +785,10 @@ struct Block {
   void window_mark(long long it);
   void window_drain();
   void wait_event(cudaEvent_t e);
-  [[noreturn]] void on_timeout();
+  // in-process peers: returns once `word` of peer r's progress reaches `want`
+  void wait_host(int r, const std::atomic<unsigned long long> HostProgress::*word, unsigned long long want,
+                 long long it);
+  [[noreturn]] void on_timeout(long long hint = 0);
 };
 
 Block::Block(const cav_block_desc& desc) : d(desc) {
@@ -888,9 +945,16 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   peer_arena.assign(d.np, nullptr);
   peer_ipc.assign(d.np, false);
   peer_arena[d.rank] = arena;
+  host_peer.assign(d.np, nullptr);
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  registry()[arena] = prog;
 }
 
 Block::~Block() {
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    registry().erase(arena);
+  }
   cudaSetDevice(d.device);
   if (s0) cudaStreamSynchronize(s0);
   if (s1) cudaStreamSynchronize(s1);
@@ -1007,7 +1071,10 @@ void Block::launch_fold(long long it) {
   const unsigned long long want = base() + static_cast<unsigned long long>(it);
   Slot* mine = reinterpret_cast<Slot*>(arena + lay.slots);
   std::vector<std::pair<const unsigned long long*, unsigned long long>> w;
-  for (int r = 0; r < d.np; ++r) w.emplace_back(&mine[r * 2 + par].stamp, want);
+  for (int r = 0; r < d.np; ++r) {
+    wait_host(r, &HostProgress::push, base() + static_cast<unsigned long long>(it - 1), it);
+    w.emplace_back(&mine[r * 2 + par].stamp, want);
+  }
   stream_wait_geq(s0, w, wait_flags);
   FoldArgs a{};
   a.slots = mine;
@@ -1045,6 +1112,7 @@ void Block::launch_push(long long it) {
   a.abort = abort_flag;
   k_push<<<1, 32, 0, s0>>>(a);
   CAV_CUDA(cudaGetLastError());
+  prog->push.store(base() + static_cast<unsigned long long>(it), std::memory_order_release);
 }
 
 void Block::launch_step(int part, long long it, bool check, unsigned long long* dig) {
@@ -1194,6 +1262,8 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
     x.msg = d_pack;
     k_pack<<<xgrid, kXThreads, 0, xs>>>(x);
     CAV_CUDA(cudaGetLastError());
+    prog->pack.store(x.val, std::memory_order_release);
+    for (const auto& e : plan) wait_host(e.neighbor, &HostProgress::pack, x.val, it);
     stream_wait_geq(xs, fw, wait_flags);
     x.msg = d_unpack;
     k_unpack<<<xgrid, kXThreads, 0, xs>>>(x);
@@ -1257,6 +1327,20 @@ void Block::wait_event(cudaEvent_t e) {
   }
 }
 
+void Block::wait_host(int r, const std::atomic<unsigned long long> HostProgress::*word, unsigned long long want,
+                      long long it) {
+  const HostProgress* p = host_peer[r].get();
+  if (!p || r == d.rank || (p->*word).load(std::memory_order_acquire) >= want) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  const double lim = d.timeout_ms > 0 ? d.timeout_ms : 20000.0;
+  for (int spin = 0; (p->*word).load(std::memory_order_acquire) < want; ++spin) {
+    if (std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() > lim)
+      on_timeout(it);
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(5));
+    else std::this_thread::yield();
+  }
+}
+
 void Block::window_mark(long long it) {
   if (d.np == 1) return;
   const int q = static_cast<int>(it % kWindow);
@@ -1278,14 +1362,14 @@ void Block::window_drain() {
   for (auto& w : win_it) w = 0;
 }
 
-void Block::on_timeout() {
+void Block::on_timeout(long long hint) {
   // the first iteration that has not completed is the stuck one
   long long stuck = 0;
   for (int q = 0; q < kWindow; ++q)
     if (win_it[q] > 0 && cudaEventQuery(win[q]) != cudaSuccess && (stuck == 0 || win_it[q] < stuck))
       stuck = win_it[q];
   cudaGetLastError();
-  if (stuck == 0) stuck = next_n;
+  if (stuck == 0) stuck = hint > 0 ? hint : next_n;
   // what this rank still waits for, read from its arena on the side stream
   std::vector<unsigned long long> flags(64);
   std::vector<Slot> slots(2 * d.np);
@@ -1401,6 +1485,9 @@ int cav_block_connect(cav_block* bh, int r, void* ptr, const unsigned char* ipc)
         cudaGetLastError();
       }
       b.peer_arena[r] = static_cast<unsigned char*>(ptr);
+      std::lock_guard<std::mutex> lk(g_reg_mu);
+      const auto f = registry().find(ptr);
+      b.host_peer[r] = f == registry().end() ? nullptr : f->second;  // same process: order the waits
     } else {
       cudaIpcMemHandle_t h;
       std::memcpy(&h, ipc, 64);

@@ -260,22 +260,10 @@ int cav_run_case(const cav_run_config* cfg, const cav_case_options* opt, cav_cas
     if (cfg->np < 1 || cfg->np > 512) throw std::invalid_argument("run: np must be in 1..512");
     const auto dims = host::decomp_dims(cfg->np, cfg->mode, cfg->dims);
     host::cavity_spacing(cfg->nx, cfg->ny, cfg->nz, cfg->fluid.length, cfg->fluid.length, cfg->fluid.length);
-    // Ranks sharing a GPU each drive 3 streams, two of which wait (stream
-    // memory operations) for work of other ranks; CUDA multiplexes streams
-    // onto CUDA_DEVICE_MAX_CONNECTIONS hardware queues (default 8), and two
-    // streams on one queue would serialise a waiter ahead of the work it
-    // waits for.
-    {
-      int per_dev[8] = {};
-      for (int r = 0; r < cfg->np; ++r) ++per_dev[cfg->devices[r % 8] & 7];
-      int most = 0;
-      for (int d = 0; d < 8; ++d) most = std::max(most, per_dev[d]);
-      const char* env = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
-      const int conns = env ? std::atoi(env) : 8;
-      if (most > 1 && 3 * most > conns)
-        throw std::invalid_argument("run: " + std::to_string(most) + " ranks share one GPU; set CUDA_DEVICE_MAX_CONNECTIONS >= " +
-                                    std::to_string(3 * most) + " (max 32) before CUDA initialises");
-    }
+    // Ranks sharing a GPU may have their streams multiplexed onto the same
+    // hardware queues (CUDA_DEVICE_MAX_CONNECTIONS); blocks enqueue every
+    // cross-rank wait only after its producer (HostProgress, block.cu), so
+    // any mapping is deadlock-free.
     Shared sh(cfg, opt, cfg->np);
     sh.gn = {cfg->nx, cfg->ny, cfg->nz};
     sh.dims = dims;

@@ -5,7 +5,6 @@ export PYTHONUNBUFFERED=1
 TAG=${1:-t}
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 echo "smoke exit $?"
-if [ -n "$2" ]; then K="-k $2"; else K=""; fi
-timeout 2400 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider $K --durations=15 > gpurun_out/pytest_gpu_$TAG.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider ${2:+-k "$2"} --durations=15 > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo "pytest exit $?"
 tail -5 gpurun_out/pytest_gpu_$TAG.log

@@ -85,3 +85,29 @@ int main() {
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines()
     assert out[0].startswith("choose_dims: 2d cannot split a prime rank count 7")
     assert out[1] == "2 2 2"
+
+
+def test_ctypes_prototypes_match_header():
+    """Every argtypes list capi.py declares has the arity of the header's
+    prototype (a stale list turns a call into a TypeError on the GPU box)."""
+    import re
+    from paper_2006_02602_b200 import capi
+    src = open(os.path.join(ROOT, "include", "cavity_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    protos = {}
+    for m in re.finditer(r"\b(?:int|void|double|const char\*)\s+(cav_\w+)\s*\(([^;{]*?)\)\s*;", src, flags=re.S):
+        args = m.group(2).strip()
+        depth, n = 0, (0 if args in ("", "void") else 1)
+        for ch in args:
+            depth += ch in "([" and 1 or 0
+            depth -= ch in ")]" and 1 or 0
+            n += ch == "," and depth == 0
+        protos[m.group(1)] = n
+    L = capi.lib()
+    checked = 0
+    for name, n in protos.items():
+        at = getattr(getattr(L, name), "argtypes", None)
+        if at is not None:
+            assert len(at) == n, (name, len(at), n)
+            checked += 1
+    assert checked >= 10

@@ -133,10 +133,57 @@ def test_linf_norm_matches_numpy_over_oracle_residuals(monkeypatch, kw, env):
 
 def test_device_converged_solve_stored_ghosts(monkeypatch):
     monkeypatch.setenv("CAV_STORED_GHOSTS", "1")
-    cfg = capi.default_config(grid=(20, 16, 12), steps=-1, conv_tol=1e-3)
+    cfg = capi.default_config(grid=(32, 32, 32), steps=-1)  # configs[0]: converges at ~6600
     r = capi.run_case(cfg, collect_fields=True, collect_history=True)
     o = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
     assert r.converged and o["converged"] and r.steps_marched == o["steps_marched"]
     np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
     assert r.ledgers[0]["exchanges"] == r.steps_marched  # no ledger entries for the no-op tail
+
+
+def test_gpu_scaling_series_csv(tmp_path):
+    """run_bench on the GPU path (src/bench.cpp:18-75): strong and weak series
+    in the reference's RunRecord CSV, validated, speedups filled against np=1,
+    plus the B200 sidecar columns."""
+    from paper_2006_02602_b200 import records, series
+    for scaling in ("strong", "weak"):
+        ser, extra, warn = series.run_series((24, 24, 24), [1, 2, 4], ["3d"], scaling=scaling, steps=6, warmup=2)
+        assert not warn and len(ser) == 1 and [r.np for r in ser[0].rows] == [1, 2, 4]
+        paths = series.write_outputs(ser, extra, str(tmp_path), scaling)
+        rows = records.parse_csv(open(paths[0]).read())
+        assert [r.np for r in rows] == [1, 2, 4]
+        assert rows[0].speedup == 1.0 and rows[0].efficiency == 1.0
+        assert all(r.ssspnt > 0 and r.steps == 6 for r in rows)
+        if scaling == "weak":
+            assert [r.size for r in rows] == [24 ** 3, 2 * 24 ** 3, 4 * 24 ** 3]
+        side = open(paths[1]).read().splitlines()
+        assert side[0] == series.EXTRA_HEADER and len(side) == 4
+        assert all(0.0 < e["roofline_frac"] < 1.5 and e["exposed_comm_frac"] >= 0.0 for e in extra)
+
+
+def test_ranks_on_one_hardware_queue():
+    """Every stream of every in-process rank multiplexed onto ONE hardware
+    queue (CUDA_DEVICE_MAX_CONNECTIONS=1, set before CUDA initialises in a
+    fresh process): cross-rank waits are enqueued only after their
+    producers, so even a single FIFO cannot deadlock; results stay bitwise."""
+    import subprocess
+    import sys
+    import os
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2006_02602_b200 import capi
+from oracle.refbind import Oracle
+for kw in (dict(np=4, mode="2d", strategy="v3", overlap=1), dict(np=3, mode="1d-j", strategy="v2", overlap=0),
+           dict(np=8, mode="3d", strategy="baseline", overlap=1)):
+    base = dict(grid=(26, 22, 18), steps=25, check_every=5)
+    r = capi.run_case(capi.default_config(**base, **kw), collect_fields=True, collect_history=True)
+    o = Oracle.run_case(capi.default_config(**base), collect_fields=True, collect_history=True)
+    assert np.array_equal(r.fields.view(np.uint64), o["fields"].view(np.uint64)), kw
+    assert np.array_equal(r.history.view(np.uint64), o["history"].view(np.uint64)), kw
+print("ONE-QUEUE-OK")
+""".format(root=os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="1")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    assert p.returncode == 0 and "ONE-QUEUE-OK" in p.stdout, p.stdout + p.stderr
