@@ -2,23 +2,29 @@
 // the B200-native replacement of rank_main's loop body
 // (/root/reference/proj/src/runner.cpp:184-235).
 //
-// Iteration n on rank r (all on the block's stream unless overlapping):
-//   K1 bc        wall ghosts of state A from the lazily shifted interior
-//                (apply_boundary_conditions, src/solver.cpp:158-191)
-//   K2 pack      plan entries of A pushed straight into the neighbours'
-//                receive slabs over NVLink/peer memory, release flag per entry
-//                (exchange_begin, src/exchange.cpp:115-145)
-//   K3 unpack    acquire flag, scatter into A's join ghosts
-//                (exchange_finish, src/exchange.cpp:147-176)
-//   K4 step      fused: residual + [exact norm digits] + Euler update into B
-//                + next-step CFL maxima + non-finite flags + centre pressure
-//                (compute_residual, global_norms, compute_dt, euler_step,
-//                center_pressure_broadcast; src/runner.cpp:196-228)
-//   K6 sync      push (maxima, pc, err) to every rank's slot, wait for all,
-//                fold dt_{n+1} and pc_n (reduce_fixed_order(Min) and
-//                broadcast_double, src/transport.cpp:23-60); replaces barrier()
-// The rescale p -= pc_n is never a separate pass: every consumer of A applies
-// fl(p - pc_{n-1}) when it loads an interior pressure.
+// Iteration n on rank r. Compute stream s0; the halo exchange runs on s1
+// when overlapping (src/runner.cpp:189-194), else on s0:
+//   pack     k_pack: plan entries of S_{n-1} stored straight into the
+//            neighbours' receive slabs over NVLink/peer memory, one release
+//            flag per entry (exchange_begin, src/exchange.cpp:115-145)
+//   unpack   stream wait on the flags (cuStreamBatchMemOp, no SM occupied),
+//            then k_unpack into the join ghosts (exchange_finish, :147-176)
+//   fold     stream wait on every rank's scalar slot of n-1; every CTA of
+//            the step then folds dt_n (reduce_fixed_order(Min),
+//            src/transport.cpp:23-60, as the exact max rewrite) and pcs_n =
+//            p'(centre) of step n from the gathered centre stencil
+//            (center_pressure_broadcast)
+//   step     k_step_tma: BC (register or stored wall ghosts) + residual +
+//            [exact norm digits] + Euler update + eager rescale fl(p'-pcs_n)
+//            + next-step CFL maxima + non-finite flags; internal items, then
+//            (after the halos landed) shell items when overlapping
+//   ghosts   k_ghosts_yz: y/z wall ghosts of S_n (stored-ghost blocks)
+//   push     the step's last CTA (k_push before iteration 1): this rank's
+//            maxima, error code and its share of S_n's centre stencil into
+//            every rank's slot, release stamp
+// One rank: the step kernel's last CTA folds dt and pcs itself (no fold or
+// push). Every cross-rank wait is enqueued only after the launch that
+// produces its value has been enqueued (HostProgress below).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -151,153 +157,13 @@ __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Scalars between ranks (reduce_fixed_order(Min) of dt and the centre
-// pressure broadcast, src/transport.cpp:23-60, src/exchange.cpp:183-193),
-// folded so that one exchange per iteration suffices and every block can
-// store its rescaled pressure eagerly:
-//   k_push (after step n): this rank's CFL maxima and error code, plus the
-//     values of S_n it owns among the centre cell's stencil (the 13-point p
-//     star and the u, v, w values R_p reads), into slot[rank][n&1] of every
-//     rank's arena, then a release of the slot's stamp;
-//   k_fold (before step n+1, after the stream waited for every stamp):
-//     dt_{n+1} from the global maxima (the exact max rewrite of compute_dt)
-//     and pcs_{n+1} = p'(centre) of step n+1 from the gathered star — the
-//     residual and update of that one cell with the step's own arithmetic —
-//     so step n+1 stores fl(p' - pcs_{n+1}) exactly as rescale_pressure
-//     (src/solver.cpp:248-257) would leave it.
-// Star order: p, p-x, p+x, p-2x, p+2x, p-y, p+y, p-2y, p+2y, p-z, p+z, p-2z,
-// p+2z, u, u-x, u+x, v, v-y, v+y, w, w-z, w+z.
-constexpr int kStar = 22;
-struct Slot {
-  unsigned long long d[3];
-  unsigned long long err;
-  unsigned long long stamp;
-  unsigned long long pad[3];
-  double star[24];
-};
-static_assert(sizeof(Slot) == 256, "slot size");
-
-struct StarCells {       // this rank's share of the centre star
-  int n;
-  int slot[kStar];
-  int var[kStar];
-  long long idx[kStar];  // storage index within the field
-};
-
-struct PushArgs {
-  const Acc* acc;
-  const double* state;   // S_n (the step's output)
-  long long fstride;
-  StarCells mine;
-  Slot* const* peer_slots;
-  int np, rank, par;
-  unsigned long long stamp;
-  const int* abort;
-};
-
-__global__ void __launch_bounds__(32) k_push(const PushArgs a) {
-  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
-  __shared__ double st[kStar];
-  const int t = threadIdx.x;
-  if (t < kStar) st[t] = 0.0;
-  __syncwarp();
-  if (t < a.mine.n) st[a.mine.slot[t]] = a.state[a.mine.var[t] * a.fstride + a.mine.idx[t]];
-  __syncwarp();
-  const Acc mine = *a.acc;
-  for (int r = t; r < a.np; r += 32) {
-    Slot* s = a.peer_slots[r] + (a.rank * 2 + a.par);
-    s->d[0] = mine.dmax[0];
-    s->d[1] = mine.dmax[1];
-    s->d[2] = mine.dmax[2];
-    s->err = mine.err;
-    for (int q = 0; q < kStar; ++q) s->star[q] = st[q];
-    __threadfence_system();
-    st_release_sys(&s->stamp, a.stamp);
-  }
-}
-
-struct FoldArgs {
-  const Slot* slots;     // this rank's arena: Slot[np][2]
-  int np, par;
-  unsigned long long stamp;
-  int owner[kStar];      // rank holding each star value
-  int rescale;
-  IterScalars* sc;       // this iteration's scalars
-  Acc* acc;              // this iteration's accumulators (reset)
-  double dx, dy, dz, cfl;
-  cav_fluid_params fl;
-  cav_stencil_params sp;
-  BetaFast bf;
-  unsigned long long* err_sticky;
-  const int* abort;
-};
-
-constexpr int kFoldThreads = 128;
-
-__global__ void __launch_bounds__(kFoldThreads) k_fold(const FoldArgs a) {
-  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
-  __shared__ unsigned long long sd[3][kFoldThreads], se[kFoldThreads];
-  const int t = threadIdx.x;
-  unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
-  for (int r = t; r < a.np; r += kFoldThreads) {
-    const Slot* s = a.slots + (r * 2 + a.par);
-    if (ld_acquire_sys(&s->stamp) < a.stamp) continue;  // only after an abort released the wait
-    d0 = max(d0, __ldcg(&s->d[0]));
-    d1 = max(d1, __ldcg(&s->d[1]));
-    d2 = max(d2, __ldcg(&s->d[2]));
-    e = min(e, __ldcg(&s->err));
-  }
-  sd[0][t] = d0;
-  sd[1][t] = d1;
-  sd[2][t] = d2;
-  se[t] = e;
-  __syncthreads();
-  if (t != 0) return;
-  for (int q = 1; q < kFoldThreads; ++q) {
-    d0 = max(d0, sd[0][q]);
-    d1 = max(d1, sd[1][q]);
-    d2 = max(d2, sd[2][q]);
-    e = min(e, se[q]);
-  }
-  const unsigned long long dm[3] = {d0, d1, d2};
-  const double dt = ops::dt_from_maxima(dm, a.dx, a.dy, a.dz, a.fl, a.cfl);
-  double pcs = 0.0;
-  if (a.rescale) {
-    double v[kStar];
-    for (int q = 0; q < kStar; ++q) v[q] = __ldcg(&a.slots[a.owner[q] * 2 + a.par].star[q]);
-    Star s{};
-    s.p = v[0];
-    s.pxm = v[1];
-    s.pxp = v[2];
-    s.pxm2 = v[3];
-    s.pxp2 = v[4];
-    s.pym = v[5];
-    s.pyp = v[6];
-    s.pym2 = v[7];
-    s.pyp2 = v[8];
-    s.pzm = v[9];
-    s.pzp = v[10];
-    s.pzm2 = v[11];
-    s.pzp2 = v[12];
-    s.u = v[13];
-    s.uxm = v[14];
-    s.uxp = v[15];
-    s.v = v[16];
-    s.vym = v[17];
-    s.vyp = v[18];
-    s.w = v[19];
-    s.wzm = v[20];
-    s.wzp = v[21];
-    // center_p_update's arithmetic (R_p reads only these values)
-    pcs = s.p + dt * residual_of(s, a.sp, a.bf).p;
-  }
-  a.sc->dt = dt;
-  a.sc->pc = 0.0;
-  a.sc->pcs = pcs;
-  Acc z{};
-  z.err = ~0ull;
-  *a.acc = z;
-  if (e < *a.err_sticky) *a.err_sticky = e;
+// Scalars between ranks: see step_tma.cuh (fold_scalars_warp / push_scalars_warp).
+// Iteration 0's push (the initial state's maxima and centre stencil) has no
+// step kernel to ride on, so it is this one-thread kernel.
+__global__ void __launch_bounds__(32) k_push(const XDesc* x, int par, unsigned long long stamp, const Acc* acc,
+                                             const double* state, long long fs, const int* abort) {
+  if (*reinterpret_cast<const volatile int*>(abort)) return;
+  push_scalars_warp(x, par, stamp, acc, state, fs);
 }
 
 // Whole-storage export in the reference Field3 layout: interior from `cur`
@@ -433,36 +299,18 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
     const long long fs = g.fstride, plane = static_cast<long long>(g.pitch) * g.ypitch;
     const int k1 = min(k0 + kNormRunSeg, b.hi[2]);
     const double* q = rs + g.idx(i, j, k0);
-    // two planes in flight ahead of the two being summed (the loads do not
-    // depend on the digit-run arithmetic; without the explicit lookahead the
-    // kernel was latency-bound at ~1.9 TB/s)
-    auto load = [&](double* x, int k) {
-      if (k < k1) {
+    // (measured: an explicit two-plane lookahead of the loads, 100 registers,
+    // made the norm iteration slower, 0.78 -> 0.94 ms at 256^3)
+    for (int k = k0; k < k1; ++k, q += plane) {
+      double x[5];
 #pragma unroll
-        for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + (k - k0) * plane + v * fs);
-      }
-    };
-    auto add = [&](const double* x) {
+      for (int v = 0; v < 5; ++v) x[v] = __ldcs(q + v * fs);
 #pragma unroll
       for (int v = 0; v < 5; ++v) {
         mx[v] = max(mx[v], abs_bits(x[v]));
         const double x2 = x[v] * x[v];
         if (nonfinite(x2)) nf = 1;
         else digit_run_add(runs[v], sd + v * kDigits, x2);
-      }
-    };
-    double a0[5], a1[5], b0[5], b1[5];
-    load(a0, k0);
-    load(a1, k0 + 1);
-    for (int k = k0; k < k1; k += 2) {
-      load(b0, k + 2);
-      load(b1, k + 3);
-      add(a0);
-      if (k + 1 < k1) add(a1);
-#pragma unroll
-      for (int v = 0; v < 5; ++v) {
-        a0[v] = b0[v];
-        a1[v] = b1[v];
       }
     }
 #pragma unroll
@@ -729,6 +577,7 @@ struct Block {
   MsgDesc* d_pack = nullptr;
   MsgDesc* d_unpack = nullptr;
   Slot** d_peer_slots = nullptr;
+  XDesc* d_xd = nullptr;         // cross-rank scalar constants (step_tma.cuh)
   unsigned long long* digits = nullptr;
   ConvState* conv = nullptr;              // device convergence state (single rank)
   const int* stop_flag = nullptr;         // = &conv->stop while a device-converging run is active
@@ -761,7 +610,7 @@ struct Block {
   int tail_chunks = -1;          // CAV_TAIL_CHUNKS: short chunks at the end (-1 = two waves)
   int tma_chunk = 0;             // CAV_TMA_CHUNK: fixed k-chunk (0 = balanced choice)
   WallInfo winfo{};
-  int tma_grid = 0;
+  int tma_grid = 0;      // persistent step grid: CTAs per SM x SMs
   int shell[4] = {0, 0, 0, 0};   // internal tile range sx0, sx1, sy0, sy1
   int zsh[2] = {0, 0};           // joined low / high z faces
   StarCells star_mine{};
@@ -775,8 +624,10 @@ struct Block {
   void ensure_ready();
   void prologue();
   void iteration(long long it, bool check, unsigned long long* dig, IterTiming* tm);
-  void launch_step(int part, long long it, bool check, unsigned long long* dig);
-  void launch_fold(long long it);
+  // returns the launch's item count; dry: only count
+  long long launch_step(int part, long long it, bool check, unsigned long long* dig, bool xfold, bool write_sc,
+                        bool push, bool dry);
+  void wait_scalars(long long it);
   void launch_push(long long it);
   void launch_ghosts();
   void update_ledger(cav_ledger& l) const;
@@ -871,7 +722,6 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_pack));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_unpack));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_push));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_fold));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_export));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_fill_ic));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_import));
@@ -932,6 +782,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaMalloc(&conv, sizeof(ConvState)));
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
+  CAV_CUDA(cudaMalloc(&d_xd, sizeof(XDesc)));
   if (!plan.empty()) {
     CAV_CUDA(cudaMalloc(&d_pack, plan.size() * sizeof(MsgDesc)));
     CAV_CUDA(cudaMalloc(&d_unpack, plan.size() * sizeof(MsgDesc)));
@@ -975,6 +826,7 @@ Block::~Block() {
   cudaFree(counters);
   cudaFree(conv);
   cudaFree(d_peer_slots);
+  cudaFree(d_xd);
   cudaFree(d_pack);
   cudaFree(d_unpack);
   if (digits) cudaFreeAsync(digits, s0);
@@ -997,6 +849,23 @@ void Block::ensure_ready() {
   std::vector<Slot*> ps(d.np);
   for (int r = 0; r < d.np; ++r) ps[r] = reinterpret_cast<Slot*>(peer_arena[r] + lay.slots);
   CAV_CUDA(cudaMemcpyAsync(d_peer_slots, ps.data(), d.np * sizeof(Slot*), cudaMemcpyHostToDevice, s0));
+  XDesc xd{};
+  xd.slots = reinterpret_cast<const Slot*>(arena + lay.slots);
+  xd.peer_slots = d_peer_slots;
+  xd.np = d.np;
+  xd.rank = d.rank;
+  xd.rescale = d.rescale;
+  for (int q = 0; q < kStar; ++q) xd.owner[q] = static_cast<signed char>(star_owner[q]);
+  xd.mine = star_mine;
+  xd.sp = sp;
+  xd.bf = bf;
+  xd.dx = dx;
+  xd.dy = dy;
+  xd.dz = dz;
+  xd.cfl = d.cfl;
+  xd.nu = d.fluid.nu;
+  xd.alpha = d.fluid.alpha;
+  CAV_CUDA(cudaMemcpyAsync(d_xd, &xd, sizeof xd, cudaMemcpyHostToDevice, s0));
   std::vector<MsgDesc> pk(plan.size()), up(plan.size());
   for (size_t m = 0; m < plan.size(); ++m) {
     const cav_plan_entry& e = plan[m];
@@ -1065,58 +934,29 @@ void Block::prologue() {
   primed = true;
 }
 
-void Block::launch_fold(long long it) {
-  // every rank's push of iteration it-1
+void Block::wait_scalars(long long it) {
+  // every rank's push of iteration it-1: enqueued (in-process peers), then
+  // landed (stream wait on the stamps, no SM held)
+  const Slot* slots = reinterpret_cast<const Slot*>(arena + lay.slots);
   const int par = static_cast<int>((it - 1) & 1);
-  const unsigned long long want = base() + static_cast<unsigned long long>(it);
-  Slot* mine = reinterpret_cast<Slot*>(arena + lay.slots);
   std::vector<std::pair<const unsigned long long*, unsigned long long>> w;
   for (int r = 0; r < d.np; ++r) {
     wait_host(r, &HostProgress::push, base() + static_cast<unsigned long long>(it - 1), it);
-    w.emplace_back(&mine[r * 2 + par].stamp, want);
+    w.emplace_back(&slots[r * 2 + par].stamp, base() + static_cast<unsigned long long>(it));
   }
   stream_wait_geq(s0, w, wait_flags);
-  FoldArgs a{};
-  a.slots = mine;
-  a.np = d.np;
-  a.par = par;
-  a.stamp = want;
-  for (int q = 0; q < kStar; ++q) a.owner[q] = star_owner[q];
-  a.rescale = d.rescale;
-  a.sc = sc + (it & 1);
-  a.acc = acc + (it & 1);
-  a.dx = dx;
-  a.dy = dy;
-  a.dz = dz;
-  a.cfl = d.cfl;
-  a.fl = d.fluid;
-  a.sp = sp;
-  a.bf = bf;
-  a.err_sticky = err;
-  a.abort = abort_flag;
-  k_fold<<<1, kFoldThreads, 0, s0>>>(a);
-  CAV_CUDA(cudaGetLastError());
 }
 
-void Block::launch_push(long long it) {
-  PushArgs a{};
-  a.acc = acc + (it & 1);
-  a.state = state[it == 0 ? cur : cur ^ 1];  // S_it: the step's output (the initial state for it == 0)
-  a.fstride = g.fstride;
-  a.mine = star_mine;
-  a.peer_slots = d_peer_slots;
-  a.np = d.np;
-  a.rank = d.rank;
-  a.par = static_cast<int>(it & 1);
-  a.stamp = base() + static_cast<unsigned long long>(it) + 1;
-  a.abort = abort_flag;
-  k_push<<<1, 32, 0, s0>>>(a);
+void Block::launch_push(long long it) {  // iteration 0 only (later pushes ride on the step kernel)
+  k_push<<<1, 32, 0, s0>>>(d_xd, static_cast<int>(it & 1), base() + static_cast<unsigned long long>(it) + 1,
+                           acc + (it & 1), state[cur], g.fstride, abort_flag);
   CAV_CUDA(cudaGetLastError());
   prog->push.store(base() + static_cast<unsigned long long>(it), std::memory_order_release);
 }
 
-void Block::launch_step(int part, long long it, bool check, unsigned long long* dig) {
-  step_used_scratch = false;
+long long Block::launch_step(int part, long long it, bool check, unsigned long long* dig, bool xfold, bool write_sc,
+                              bool push, bool dry) {
+  if (!dry) step_used_scratch = false;
   TmaStepArgs a{};
   a.out = state[cur ^ 1];
   a.g = g;
@@ -1185,20 +1025,32 @@ void Block::launch_step(int part, long long it, bool check, unsigned long long* 
   // three interior layers next to each x wall lie in one warp (one 32-wide
   // tile row); k_ghosts_yz writes the y and z faces after it (k_bc all faces otherwise)
   a.gw = ghosts && ghost_writes && bw >= 3 && (bw % 32 == 0 || bw % 32 >= 3) ? 1 : 0;
-  if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
-    a.rs = rscratch;
-    step_used_scratch = true;
-  }
-  step_wrote_ghosts = a.gw != 0;
   const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
   long long wanted = total;
   if (a.part != 0) {
     const long long internal = static_cast<long long>(a.nchunks - a.zl - a.zh) * (a.sx1 - a.sx0) * (a.sy1 - a.sy0);
     wanted = a.part == 1 ? internal : total - internal;
   }
-  if (wanted <= 0) return;
+  if (dry || wanted <= 0) return wanted;
+  if (ghosts && check) {  // norm iteration: residuals to the scratch state, summed by k_norm_runs
+    a.rs = rscratch;
+    step_used_scratch = true;
+  }
+  step_wrote_ghosts = a.gw != 0;
+  if (xfold) {  // many ranks: dt/pcs folded in the kernel, scalars pushed by its last CTA
+    a.xd = d_xd;
+    a.xfold = 1;
+    a.write_sc = write_sc ? 1 : 0;
+    a.fold_par = static_cast<int>((it - 1) & 1);
+    a.fold_stamp = base() + static_cast<unsigned long long>(it);
+    a.xpush = push ? 1 : 0;
+    a.push_par = static_cast<int>(it & 1);
+    a.push_stamp = base() + static_cast<unsigned long long>(it) + 1;
+  }
   const int grid = static_cast<int>(std::min<long long>(tma_grid, wanted));
   tma_launch<TmaV0>(tmap[cur], a, check, ghosts, grid, s0);
+  if (push) prog->push.store(base() + static_cast<unsigned long long>(it), std::memory_order_release);
+  return wanted;
 }
 
 void Block::launch_ghosts() {
@@ -1220,15 +1072,10 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
   auto mark = [&](int q, cudaStream_t st) {
     if (tm) CAV_CUDA(cudaEventRecord(tm->e[q], st));
   };
-  if (d.np == 1) {  // the step kernel's last CTA folds the scalars
-    mark(0, s0);
-    mark(1, s0);
+  if (d.np == 1) {  // the step kernel's last CTA folds the scalars (timing: e[2], e[3] only)
     mark(2, s0);
-    launch_step(0, it, check, dig);
+    launch_step(0, it, check, dig, false, false, false, false);
     mark(3, s0);
-    mark(4, s0);
-    mark(5, s0);
-    mark(6, s0);
     if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, stop_flag, s0);
     launch_ghosts();
     cur ^= 1;
@@ -1269,32 +1116,34 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
     k_unpack<<<xgrid, kXThreads, 0, xs>>>(x);
     CAV_CUDA(cudaGetLastError());
   };
-  if (ov) exchange();  // on s1, concurrent with the fold and the internal items
+  if (ov) exchange();  // on s1, concurrent with the internal items
   mark(0, s0);
-  launch_fold(it);  // waits for every rank's scalars of iteration it-1
+  wait_scalars(it);  // every rank's scalars of iteration it-1
   mark(1, s0);
   if (ov) {
     CAV_CUDA(cudaEventRecord(ev_join, s1));
     // overlap (src/runner.cpp:189-194): internal items while the halos
-    // travel, then the shell items once they landed
+    // travel, then the shell items once they landed. The first launch with
+    // items stores the folded scalars, the last one pushes.
+    const bool has1 = launch_step(1, it, check, dig, true, false, false, true) > 0;
+    const bool has2 = launch_step(2, it, check, dig, true, false, false, true) > 0;
     mark(2, s0);
-    launch_step(1, it, check, dig);
+    if (has1) launch_step(1, it, check, dig, true, true, !has2, false);
     mark(3, s0);
     CAV_CUDA(cudaStreamWaitEvent(s0, ev_join, 0));
     mark(4, s0);
-    launch_step(2, it, check, dig);
+    if (has2) launch_step(2, it, check, dig, true, !has1, true, false);
     mark(5, s0);
   } else {
     exchange();
     mark(2, s0);
-    launch_step(0, it, check, dig);
+    launch_step(0, it, check, dig, true, true, true, false);
     mark(3, s0);
     mark(4, s0);
     mark(5, s0);
   }
   if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, abort_flag, s0);
   launch_ghosts();
-  launch_push(it);
   mark(6, s0);
   cur ^= 1;
 }
@@ -1704,7 +1553,7 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   // step (two launches when overlapping), [ghosts after a stored-ghost step], [k_norm_runs]
   int n = (b.d.np > 1 && b.d.overlap ? 2 : 1) + (b.ghosts && (yz || !b.ghost_writes) && walls ? 1 : 0) +
           (check && b.ghosts ? 1 : 0);
-  if (b.d.np > 1) n += 2 + (b.plan.empty() ? 0 : 2);  // fold, push, [pack, unpack]
+  if (b.d.np > 1) n += b.plan.empty() ? 0 : 2;  // pack, unpack (fold and push ride on the step kernel)
   return n;
 }
 
@@ -1748,6 +1597,7 @@ int cav_block_bench(cav_block* bh, long long n_its, double out[3]) {
       float t = 0.f;
       CAV_CUDA(cudaEventElapsedTime(&t, e[2], e[3]));
       ks += t;
+      if (b.d.np == 1) continue;  // one launch, no peers
       CAV_CUDA(cudaEventElapsedTime(&t, e[4], e[5]));
       ks += t;
       CAV_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));  // scalar wait (+ the 1-thread fold)

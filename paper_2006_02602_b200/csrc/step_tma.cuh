@@ -136,6 +136,141 @@ struct TmaCfg {
   static_assert(R >= 5, "ring must hold planes k..k+3 plus one in flight");
 };
 
+// ---- scalars between ranks (np > 1) -----------------------------------------
+// reduce_fixed_order(Min) of dt and the centre-pressure broadcast
+// (src/transport.cpp:23-60, src/exchange.cpp:183-193), folded so that one
+// exchange per iteration suffices and every block stores its rescaled
+// pressure eagerly:
+//   push (the last CTA of iteration n's last step launch; k_push for n = 0):
+//     this rank's CFL maxima and error code, plus the values of S_n it owns
+//     among the centre cell's stencil (the 13-point p star and the u, v, w
+//     values R_p reads), into slot[rank][n&1] of every rank's arena, then a
+//     release of the slot's stamp;
+//   fold (every CTA of iteration n+1's step launches, after the stream waited
+//     for every stamp): dt_{n+1} from the global maxima (the exact max
+//     rewrite of compute_dt) and pcs_{n+1} = p'(centre) of step n+1 from the
+//     gathered star — the residual and update of that one cell with the
+//     step's own arithmetic — so the step stores fl(p' - pcs_{n+1}) exactly as
+//     rescale_pressure (src/solver.cpp:248-257) would leave it.
+// Star order: p, p-x, p+x, p-2x, p+2x, p-y, p+y, p-2y, p+2y, p-z, p+z, p-2z,
+// p+2z, u, u-x, u+x, v, v-y, v+y, w, w-z, w+z.
+constexpr int kStar = 22;
+struct Slot {
+  unsigned long long d[3];
+  unsigned long long err;
+  unsigned long long stamp;
+  unsigned long long pad[3];
+  double star[24];
+};
+static_assert(sizeof(Slot) == 256, "slot size");
+
+struct StarCells {       // this rank's share of the centre star
+  int n;
+  int slot[kStar];
+  int var[kStar];
+  long long idx[kStar];  // storage index within the field
+};
+
+// Per-block constants of the cross-rank scalars, in device memory (written
+// once when the block connects), so the kernels pass one pointer.
+struct XDesc {
+  const Slot* slots;        // this rank's arena: Slot[np][2]
+  Slot* const* peer_slots;  // every rank's Slot array
+  int np, rank, rescale;
+  signed char owner[kStar];  // rank holding each star value
+  StarCells mine;
+  cav_stencil_params sp;
+  BetaFast bf;
+  double dx, dy, dz, cfl, nu, alpha;
+};
+
+// dt_n and pcs_n from every rank's slot of iteration n-1 (parity par), by
+// one warp (all 32 lanes): lane r reads rank r's maxima and error code, lane q
+// the q-th star value; lane 0 folds. The stream waited for every stamp
+// before the launch, so plain L2 loads see the pushed values (a stamp below
+// `stamp` only remains after an abort released the wait: skipped).
+__device__ __noinline__ void fold_scalars_warp(const XDesc* x, int par, unsigned long long stamp, double* sstar,
+                                               double* out_dt, double* out_pcs, unsigned long long* out_err) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
+  for (int r = lane; r < x->np; r += 32) {
+    const Slot* s = x->slots + (r * 2 + par);
+    if (__ldcg(&s->stamp) < stamp) continue;
+    d0 = max(d0, __ldcg(&s->d[0]));
+    d1 = max(d1, __ldcg(&s->d[1]));
+    d2 = max(d2, __ldcg(&s->d[2]));
+    e = min(e, __ldcg(&s->err));
+  }
+  if (x->rescale && lane < kStar) sstar[lane] = __ldcg(&x->slots[x->owner[lane] * 2 + par].star[lane]);
+  for (int o = 16; o > 0; o >>= 1) {
+    d0 = max(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+    d1 = max(d1, __shfl_xor_sync(0xffffffffu, d1, o));
+    d2 = max(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+    e = min(e, __shfl_xor_sync(0xffffffffu, e, o));
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const unsigned long long dm[3] = {d0, d1, d2};
+  cav_fluid_params fl{};
+  fl.nu = x->nu;
+  fl.alpha = x->alpha;
+  const double dt = ops::dt_from_maxima(dm, x->dx, x->dy, x->dz, fl, x->cfl);
+  double pcs = 0.0;
+  if (x->rescale) {
+    const double* v = sstar;
+    Star s{};
+    s.p = v[0];
+    s.pxm = v[1];
+    s.pxp = v[2];
+    s.pxm2 = v[3];
+    s.pxp2 = v[4];
+    s.pym = v[5];
+    s.pyp = v[6];
+    s.pym2 = v[7];
+    s.pyp2 = v[8];
+    s.pzm = v[9];
+    s.pzp = v[10];
+    s.pzm2 = v[11];
+    s.pzp2 = v[12];
+    s.u = v[13];
+    s.uxm = v[14];
+    s.uxp = v[15];
+    s.v = v[16];
+    s.vym = v[17];
+    s.vyp = v[18];
+    s.w = v[19];
+    s.wzm = v[20];
+    s.wzp = v[21];
+    // center_p_update's arithmetic (R_p reads only these values)
+    pcs = s.p + dt * residual_of(s, x->sp, x->bf).p;
+  }
+  *out_dt = dt;
+  *out_pcs = pcs;
+  *out_err = e;
+}
+
+// This rank's scalars of iteration n (parity par) and its share of S_n's
+// centre stencil into every rank's slot, then a release of the stamp; by one
+// warp (lane r serves ranks r, r+32, ...).
+__device__ __noinline__ void push_scalars_warp(const XDesc* x, int par, unsigned long long stamp,
+                                               const volatile Acc* acc, const double* state, long long fs) {
+  const int lane = threadIdx.x & 31;
+  double st[kStar];
+  for (int q = 0; q < kStar; ++q) st[q] = 0.0;
+  for (int t = 0; t < x->mine.n; ++t) st[x->mine.slot[t]] = __ldcg(state + x->mine.var[t] * fs + x->mine.idx[t]);
+  const unsigned long long d0 = acc->dmax[0], d1 = acc->dmax[1], d2 = acc->dmax[2], err = acc->err;
+  for (int r = lane; r < x->np; r += 32) {
+    Slot* s = x->peer_slots[r] + (x->rank * 2 + par);
+    s->d[0] = d0;
+    s->d[1] = d1;
+    s->d[2] = d2;
+    s->err = err;
+    for (int q = 0; q < kStar; ++q) s->star[q] = st[q];
+    __threadfence_system();
+    st_release_sys(&s->stamp, stamp);
+  }
+}
+
 struct TmaStepArgs {
   double* out;
   Geo g;
@@ -144,7 +279,7 @@ struct TmaStepArgs {
   unsigned* work;  // dynamic item counter (items >= gridDim.x), reset by the last CTA
   const int* stop;  // set once converged (single rank) or aborted (timeout): later steps do nothing (or null)
   cav_box box;
-  const IterScalars* sc;
+  IterScalars* sc;
   Acc* acc;
   unsigned long long* digits;
   int cx, cy, cz;
@@ -178,6 +313,13 @@ struct TmaStepArgs {
   // the three interior layers lie in one warp: checked on the host); k_ghosts_yz
   // writes the y and z faces. 0: k_bc writes every face (block.cu).
   int gw;
+  // many ranks: every CTA folds dt/pcs from the slots (xfold; write_sc: CTA 0
+  // also stores them to sc and folds the peers' error codes); the last CTA of
+  // the iteration's last launch pushes (xpush) and resets acc_next
+  const XDesc* xd;
+  int xfold, write_sc, xpush;
+  int fold_par, push_par;
+  unsigned long long fold_stamp, push_stamp;
   // G norm iterations: the residuals go to this scratch state (same layout)
   // and k_norm_runs sums their squares after the step (the step's own digit
   // runs need 5 x 4 more live registers and spill at 96)
@@ -461,7 +603,27 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // are paid once per two cells.
   const int tx = lane, ty = warp;
   const Geo g = a.g;
-  const double dt = a.sc->dt, u_ref = a.sp.u_ref, pcs = a.sc->pcs;
+  double dt, pcs;
+  if (a.xfold) {
+    __shared__ double sfold[2], sstar[kStar];
+    if (warp == 0) {
+      unsigned long long e;
+      fold_scalars_warp(a.xd, a.fold_par, a.fold_stamp, sstar, &sfold[0], &sfold[1], &e);
+      if (lane == 0 && a.write_sc && blockIdx.x == 0) {
+        a.sc->dt = sfold[0];
+        a.sc->pc = 0.0;
+        a.sc->pcs = sfold[1];
+        if (e != ~0ull) atomicMin(a.err_sticky, e);
+      }
+    }
+    tma::named_sync(2, 32 * C);
+    dt = sfold[0];
+    pcs = sfold[1];
+  } else {
+    dt = a.sc->dt;
+    pcs = a.sc->pcs;
+  }
+  const double u_ref = a.sp.u_ref;
   const long long fs = g.fstride;
   const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
   const bool zlo = a.walls.wall[4], zhi = a.walls.wall[5];
@@ -728,6 +890,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     smask[warp] = bad | (nbad << 8);
   }
   tma::named_sync(1, NC);
+  bool last = false;
   if (threadIdx.x == 0) {
     unsigned mk = 0;
     for (int w = 0; w < C; ++w) {
@@ -739,7 +902,8 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     acc_publish(a.acc, m0, m1, m2, mk & 0xFF, a.n + 1, a.rank);
     if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
     __threadfence();
-    if (atomicAdd(a.done, 1u) == gridDim.x - 1) {  // every CTA has published
+    last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    if (last) {  // every CTA has published
       *a.work = 0;
       __threadfence();
       if (a.fold) {
@@ -761,6 +925,15 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         *a.acc_next = z;
       }
       *a.done = 0;
+    }
+  }
+  if (a.xpush && warp == 0 && __shfl_sync(0xffffffffu, last, 0)) {
+    // many ranks: this iteration's scalars and centre-stencil share to every rank
+    push_scalars_warp(a.xd, a.push_par, a.push_stamp, a.acc, a.out, a.g.fstride);
+    if (lane == 0) {
+      Acc z{};
+      z.err = ~0ull;
+      *a.acc_next = z;
     }
   }
   if (NORMS && !G) {
