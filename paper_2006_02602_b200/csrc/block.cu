@@ -80,6 +80,7 @@ struct XArgs {
   unsigned long long val;   // flag value of this iteration (generation | n)
   int corrupt;
   const int* abort;
+  const int* stop;  // set once the run converged (device decision) or aborted
 };
 
 constexpr int kXThreads = 256, kXItems = 4;
@@ -107,6 +108,10 @@ __device__ __forceinline__ void msg_locate(const MsgDesc& m, int q, int& v, int&
 __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
   if (*reinterpret_cast<const volatile int*>(a.abort)) return;
   const MsgDesc& m = a.msg[blockIdx.y];
+  if (*reinterpret_cast<const volatile int*>(a.stop)) {  // converged: no payload, the flag still advances
+    if (blockIdx.x == 0 && threadIdx.x == 0) st_release_sys(m.flag, a.val);
+    return;
+  }
   double* dst = m.slab + (a.n & 1) * m.scalars;
   const int base = static_cast<int>(blockIdx.x) * kXThreads * kXItems;
   if (base < m.scalars) {
@@ -137,11 +142,15 @@ __global__ void __launch_bounds__(kXThreads) k_pack(const XArgs a) {
 // the slab reads after the peer's release, then copy_box_from
 // (src/slab.cpp:54-71) into the join ghosts.
 __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
-  if (*reinterpret_cast<const volatile int*>(a.abort)) return;
+  if (*reinterpret_cast<const volatile int*>(a.abort) || *reinterpret_cast<const volatile int*>(a.stop)) return;
   const MsgDesc& m = a.msg[blockIdx.y];
   const int base = static_cast<int>(blockIdx.x) * kXThreads * kXItems;
   if (base >= m.scalars) return;
-  if (ld_acquire_sys(m.flag) < a.val) return;  // only after an abort released the wait
+  // the stream waited for the flag; the acquire also orders this CTA's slab
+  // reads after the sender's release (a lagging view waits here, an abort
+  // releases it)
+  while (ld_acquire_sys(m.flag) < a.val)
+    if (*reinterpret_cast<const volatile int*>(a.abort)) return;
   const double* src = m.slab + (a.n & 1) * m.scalars;
 #pragma unroll
   for (int it = 0; it < kXItems; ++it) {
@@ -160,10 +169,66 @@ __global__ void __launch_bounds__(kXThreads) k_unpack(const XArgs a) {
 // Scalars between ranks: see step_tma.cuh (fold_scalars_warp / push_scalars_warp).
 // Iteration 0's push (the initial state's maxima and centre stencil) has no
 // step kernel to ride on, so it is this one-thread kernel.
+// Release `v` into up to six peer words (the prologue's "my state is in
+// place" signal to each joined neighbour, fused halos).
+struct PeerWords {
+  unsigned long long* w[6];
+  int n;
+};
+__global__ void k_signal(const PeerWords p, unsigned long long v) {
+  if (threadIdx.x < p.n) {
+    __threadfence_system();
+    st_release_sys(p.w[threadIdx.x], v);
+  }
+}
+
+// The initial state's halo layers of one joined face (one layer kind) into
+// the neighbour's state (fused halos: the step kernel sends every later
+// state's halos itself): p and, for the first layer, u, v, w, T.
+__global__ void __launch_bounds__(256) k_face_send(const double* st, Geo g, const XDesc* x, int par, cav_box b,
+                                                   int m) {
+  const int w = b.hi[0] - b.lo[0], h = b.hi[1] - b.lo[1];
+  const long long nb = static_cast<long long>(w) * h * (b.hi[2] - b.lo[2]);
+  for (long long q = blockIdx.x * 256LL + threadIdx.x; q < nb; q += gridDim.x * 256LL) {
+    const int i = b.lo[0] + static_cast<int>(q % w), j = b.lo[1] + static_cast<int>((q / w) % h),
+              k = b.lo[2] + static_cast<int>(q / (static_cast<long long>(w) * h));
+    const long long c = g.idx(i, j, k), fs = g.fstride;
+    send_cell(x, par, i, j, k, m, st[c], st[c + fs], st[c + 2 * fs], st[c + 3 * fs], st[c + 4 * fs]);
+  }
+  __threadfence_system();
+}
+
 __global__ void __launch_bounds__(32) k_push(const XDesc* x, int par, unsigned long long stamp, const Acc* acc,
                                              const double* state, long long fs, const int* abort) {
   if (*reinterpret_cast<const volatile int*>(abort)) return;
   push_scalars_warp(x, par, stamp, acc, state, fs);
+}
+
+// Device convergence across ranks (the rule of src/runner.cpp:210-220 on
+// global_norms' exact sums, :81-104): after each check iteration every rank
+// pushes its exact norm digits into every rank's norm slot (parity of the
+// check count) and releases a stamp; every rank's stream waits for all
+// stamps, then k_conv_merge adds the np carry-save digit arrays word by word
+// (each word stays below 2^64: pieces are 32-bit and a global sum has far
+// fewer than 2^32 of them per digit) and applies the rule exactly as
+// k_conv_check does on one rank, so every rank takes the same decision.
+struct NormSlot {
+  unsigned long long w[CAV_NORM_WORDS];
+  unsigned long long stamp;
+  unsigned long long pad[7];
+};
+
+__global__ void __launch_bounds__(256) k_push_norms(const unsigned long long* dig, NormSlot* const* peers, int np,
+                                                    int rank, int par, unsigned long long stamp, const int* stop) {
+  const bool skip = *reinterpret_cast<const volatile int*>(stop) != 0;  // converged: stamps only
+  for (int r = blockIdx.x; r < np; r += gridDim.x) {
+    NormSlot* s = peers[r] + (rank * 2 + par);
+    if (!skip)
+      for (int q = threadIdx.x; q < CAV_NORM_WORDS; q += blockDim.x) s->w[q] = __ldcg(dig + q);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(&s->stamp, stamp);
+  }
 }
 
 // Whole-storage export in the reference Field3 layout: interior from `cur`
@@ -224,6 +289,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
   size_t slots = 0;                 // offset of Slot[np][2]
+  size_t norms = 0;                 // offset of NormSlot[np][2]
   std::vector<size_t> slab;         // per plan entry (receiver side)
   size_t bytes = 0;
 };
@@ -231,7 +297,8 @@ struct ArenaLayout {
 ArenaLayout arena_layout(const std::vector<cav_plan_entry>& plan, int np) {
   ArenaLayout L;
   L.slots = kFlagBytes;
-  size_t off = align_up(L.slots + static_cast<size_t>(np) * 2 * sizeof(Slot), 256);
+  L.norms = align_up(L.slots + static_cast<size_t>(np) * 2 * sizeof(Slot), 256);
+  size_t off = align_up(L.norms + static_cast<size_t>(np) * 2 * sizeof(NormSlot), 256);
   for (const auto& e : plan) {
     L.slab.push_back(off);
     off = align_up(off + 2 * static_cast<size_t>(e.scalars) * sizeof(double), 256);
@@ -245,6 +312,40 @@ int find_entry(const std::vector<cav_plan_entry>& plan, int face, const cav_plan
     if (plan[n].face == face && plan[n].nvars == like.nvars && plan[n].var[0] == like.var[0])
       return static_cast<int>(n);
   throw std::logic_error("exchange: no matching receive entry on the neighbour");
+}
+
+// Device geometry of a block of interior n: interior rows start 128-byte
+// aligned (off 14 -> i = 2 at 16 doubles), field stride a multiple of 32
+// doubles (TMA strides).
+Geo geo_of(const std::array<int, 3>& n) {
+  Geo g{};
+  g.nx = n[0];
+  g.ny = n[1];
+  g.nz = n[2];
+  g.off = 14;
+  g.pitch = static_cast<int>(align_up(static_cast<size_t>(g.off + n[0] + 4), 16));
+  g.ypitch = n[1] + 4;
+  g.fstride = static_cast<long long>(align_up(static_cast<size_t>(g.pitch) * g.ypitch * (n[2] + 4), 32));
+  return g;
+}
+
+// A block's device memory is ONE allocation [arena | state 0 | state 1], so
+// one pointer (in-process) or one CUDA IPC handle gives a peer both the
+// exchange arena and the states its step kernel writes halos into. Every
+// rank can compute any rank's layout from the decomposition.
+struct BlockSpan {
+  Geo g;
+  ArenaLayout lay;
+  size_t state_off = 0, state_bytes = 0, total = 0;
+};
+BlockSpan block_span(const std::array<int, 3>& n, const std::array<int, 6>& rank_at, int strategy, int np) {
+  BlockSpan b;
+  b.g = geo_of(n);
+  b.lay = arena_layout(host::build_plan(n, rank_at, strategy), np);
+  b.state_off = align_up(b.lay.bytes, 4096);
+  b.state_bytes = align_up(5 * static_cast<size_t>(b.g.fstride) * sizeof(double), 4096);
+  b.total = b.state_off + 2 * b.state_bytes;
+  return b;
 }
 
 cudaEvent_t make_event() {
@@ -371,8 +472,24 @@ __global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz(double* s, Geo g, W
   }
 }
 
-__global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal) {
-  if (threadIdx.x != 0 || c->stop) return;
+__global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal,
+                             const NormSlot* merge, int np, int par, unsigned long long stamp, const int* abort) {
+  if (c->stop) return;
+  __shared__ unsigned long long md[5 * kDigits];
+  if (merge) {  // many ranks: every rank's digits of this check, summed word by word
+    for (int r = threadIdx.x; r < np; r += blockDim.x)
+      while (ld_acquire_sys(&merge[r * 2 + par].stamp) < stamp)
+        if (*reinterpret_cast<const volatile int*>(abort)) break;
+    __syncthreads();
+    for (int q = threadIdx.x; q < 5 * kDigits; q += blockDim.x) {
+      unsigned long long w = 0;
+      for (int r = 0; r < np; ++r) w += __ldcg(&merge[r * 2 + par].w[q]);
+      md[q] = w;
+    }
+    __syncthreads();
+    dig = md;
+  }
+  if (threadIdx.x != 0) return;
   double worst = 0.0;
   for (int v = 0; v < 5; ++v) {
     const double l2 = sqrt_rn(repro_value_from_digits(dig + v * kDigits) / nglobal);  // norms_from_partials
@@ -452,38 +569,49 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw
 using TmaV0 = TmaCfg<8, 7, 2>;
 constexpr int kTY = TmaV0::TY;
 
-template <class Cfg, bool NORMS, bool G>
+template <class Cfg, bool NORMS, bool G, bool X>
 void tma_attrs() {
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G, X>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Cfg::Smem)));
-  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, NORMS, G, X>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   cudaFuncAttributes fa;
-  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, NORMS, G>));
+  CAV_CUDA(cudaFuncGetAttributes(&fa, k_step_tma<Cfg, NORMS, G, X>));
 }
 
 template <class Cfg>
 int tma_setup(int device) {
-  tma_attrs<Cfg, false, false>();
-  tma_attrs<Cfg, true, false>();
-  tma_attrs<Cfg, false, true>();
-  tma_attrs<Cfg, true, true>();
+  tma_attrs<Cfg, false, false, false>();
+  tma_attrs<Cfg, true, false, false>();
+  tma_attrs<Cfg, false, true, false>();
+  tma_attrs<Cfg, true, true, false>();
+  tma_attrs<Cfg, false, false, true>();
+  tma_attrs<Cfg, true, false, true>();
+  tma_attrs<Cfg, false, true, true>();
+  tma_attrs<Cfg, true, true, true>();
   int per_sm = 0, sms = 0;
-  CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<Cfg, false, false>, Cfg::Threads,
+  CAV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tma<Cfg, false, false, false>, Cfg::Threads,
                                                          Cfg::Smem));
   CAV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   return std::max(1, std::min(per_sm, Cfg::CTAS)) * sms;
 }
 
-template <class Cfg>
-void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, int grid, cudaStream_t st) {
+template <class Cfg, bool X>
+void tma_launch_x(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, int grid, cudaStream_t st) {
   if (ghosts) {
-    if (check) k_step_tma<Cfg, true, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
-    else k_step_tma<Cfg, false, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    if (check) k_step_tma<Cfg, true, true, X><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    else k_step_tma<Cfg, false, true, X><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
   } else {
-    if (check) k_step_tma<Cfg, true, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
-    else k_step_tma<Cfg, false, false><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    if (check) k_step_tma<Cfg, true, false, X><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    else k_step_tma<Cfg, false, false, X><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
   }
   CAV_CUDA(cudaGetLastError());
+}
+
+template <class Cfg>
+void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, bool send, int grid,
+                cudaStream_t st) {
+  if (send) tma_launch_x<Cfg, true>(m, a, check, ghosts, grid, st);
+  else tma_launch_x<Cfg, false>(m, a, check, ghosts, grid, st);
 }
 
 // Stream memory operations (driver API): a stream waits for a 64-bit value in
@@ -537,7 +665,13 @@ constexpr int kCtrAbort = 60, kCtrWork = 62, kCtrDone = 63;
 struct HostProgress {
   std::atomic<unsigned long long> push{0};  // base | it: push(it) enqueued (push(0) = +0 after prologue)
   std::atomic<unsigned long long> pack{0};  // base | it: pack(it) enqueued
+  std::atomic<unsigned long long> norm{0};  // base | c: the norm push of check c (0-based) enqueued
+  std::atomic<unsigned long long> ready{0};  // base: this run's state is in place (fused halos may land)
 };
+
+// arena words: [0, 32) halo flags of the plan entries (slab exchange),
+// [40, 46) per face: the neighbour there has initialised its run (fused halos)
+constexpr int kReadyWord = 40;
 
 std::mutex g_reg_mu;
 std::map<const void*, std::shared_ptr<HostProgress>>& registry() {
@@ -578,6 +712,8 @@ struct Block {
   MsgDesc* d_unpack = nullptr;
   Slot** d_peer_slots = nullptr;
   XDesc* d_xd = nullptr;         // cross-rank scalar constants (step_tma.cuh)
+  NormSlot** d_peer_norms = nullptr;  // every rank's NormSlot array (device convergence, np > 1)
+  long long chk_count = 0;        // check iterations since the prologue (norm slot parity)
   unsigned long long* digits = nullptr;
   ConvState* conv = nullptr;              // device convergence state (single rank)
   const int* stop_flag = nullptr;         // = &conv->stop while a device-converging run is active
@@ -605,6 +741,7 @@ struct Block {
   CUtensorMap tmap[2][2];  // [state][p, uvwT]
   BetaFast bf{-1.0, 0u};
   bool ghosts = false;           // stored wall ghosts (see launch_step)
+  bool fused = false;            // np > 1: the step kernel sends the halos itself (no pack/unpack)
   bool ghost_writes = true;      // CAV_GHOST_WRITES=0: always k_bc
   bool step_wrote_ghosts = false;  // the last step kernel wrote its output's x-wall ghosts itself
   int tail_chunks = -1;          // CAV_TAIL_CHUNKS: short chunks at the end (-1 = two waves)
@@ -677,14 +814,8 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
   CAV_CUDA(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
   CAV_CUDA(cudaStreamCreateWithFlags(&saux, cudaStreamNonBlocking));
-  // padded layout: interior rows start 128-byte aligned (off 14 -> i=2 at 16)
-  g.nx = n[0];
-  g.ny = n[1];
-  g.nz = n[2];
-  g.off = 14;
-  g.pitch = static_cast<int>(align_up(static_cast<size_t>(g.off + n[0] + 4), 16));
-  g.ypitch = n[1] + 4;
-  g.fstride = static_cast<long long>(align_up(static_cast<size_t>(g.pitch) * g.ypitch * (n[2] + 4), 32));
+  const BlockSpan span = block_span(n, rank_at, d.strategy, d.np);
+  g = span.g;
 
   // the centre cell's stencil values this rank owns (k_push) and the owner of
   // each (k_fold); the centre of a valid grid (>= 5 nodes per axis) is at
@@ -709,10 +840,10 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     }
   }
 
-  for (int s = 0; s < 2; ++s) {
-    CAV_CUDA(cudaMalloc(&state[s], 5 * g.fstride * sizeof(double)));
-    CAV_CUDA(cudaMemsetAsync(state[s], 0, 5 * g.fstride * sizeof(double), s0));
-  }
+  CAV_CUDA(cudaMalloc(&arena, span.total));
+  // Stream-ordered and completed before any peer can see this allocation.
+  CAV_CUDA(cudaMemsetAsync(arena, 0, span.total, s0));
+  for (int s = 0; s < 2; ++s) state[s] = reinterpret_cast<double*>(arena + span.state_off + s * span.state_bytes);
   // staging for upload/download, allocated once (a per-call allocation of
   // this size sat inside the e2e timed region)
   CAV_CUDA(cudaMalloc(&staging, 5 * static_cast<size_t>(n[0] + 4) * (n[1] + 4) * (n[2] + 4) * sizeof(double)));
@@ -739,6 +870,9 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     const int sg = getenv_int("CAV_STORED_GHOSTS", -1);
     ghosts = sg == 1 || (sg < 0 && static_cast<long long>(n[0]) * n[1] * n[2] >= 3000000LL);
     ghost_writes = getenv_int("CAV_GHOST_WRITES", 1) != 0;
+    // fused halos unless the corrupt-exchange hook (a receive-side test of
+    // exchange_finish) or CAV_FUSED_HALO=0 asks for the slab exchange
+    fused = d.np > 1 && !d.corrupt_exchange && getenv_int("CAV_FUSED_HALO", 1) != 0;
     tma_grid = tma_setup<TmaV0>(d.device);
     for (int s = 0; s < 2; ++s) {
       tmap[s][0] = make_state_map(state[s], g, 1, kPW, kTY + 4);
@@ -771,9 +905,6 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     wait_flags = flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0;
     batch_memop();
   }
-  CAV_CUDA(cudaMalloc(&arena, lay.bytes));
-  // Stream-ordered and completed before any peer can see this arena.
-  CAV_CUDA(cudaMemsetAsync(arena, 0, lay.bytes, s0));
   CAV_CUDA(cudaMalloc(&acc, 2 * sizeof(Acc)));
   CAV_CUDA(cudaMalloc(&sc, 2 * sizeof(IterScalars)));
   CAV_CUDA(cudaMalloc(&err, 2 * sizeof(unsigned long long)));
@@ -783,6 +914,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
   CAV_CUDA(cudaMalloc(&d_xd, sizeof(XDesc)));
+  CAV_CUDA(cudaMalloc(&d_peer_norms, d.np * sizeof(NormSlot*)));
   if (!plan.empty()) {
     CAV_CUDA(cudaMalloc(&d_pack, plan.size() * sizeof(MsgDesc)));
     CAV_CUDA(cudaMalloc(&d_unpack, plan.size() * sizeof(MsgDesc)));
@@ -815,8 +947,6 @@ Block::~Block() {
     for (auto e : t.e) cudaEventDestroy(e);
   for (auto w : win)
     if (w) cudaEventDestroy(w);
-  cudaFree(state[0]);
-  cudaFree(state[1]);
   cudaFree(staging);
   cudaFree(rscratch);
   cudaFree(arena);
@@ -827,6 +957,7 @@ Block::~Block() {
   cudaFree(conv);
   cudaFree(d_peer_slots);
   cudaFree(d_xd);
+  cudaFree(d_peer_norms);
   cudaFree(d_pack);
   cudaFree(d_unpack);
   if (digits) cudaFreeAsync(digits, s0);
@@ -849,14 +980,42 @@ void Block::ensure_ready() {
   std::vector<Slot*> ps(d.np);
   for (int r = 0; r < d.np; ++r) ps[r] = reinterpret_cast<Slot*>(peer_arena[r] + lay.slots);
   CAV_CUDA(cudaMemcpyAsync(d_peer_slots, ps.data(), d.np * sizeof(Slot*), cudaMemcpyHostToDevice, s0));
+  std::vector<NormSlot*> pn(d.np);
+  for (int r = 0; r < d.np; ++r) pn[r] = reinterpret_cast<NormSlot*>(peer_arena[r] + lay.norms);
+  CAV_CUDA(cudaMemcpyAsync(d_peer_norms, pn.data(), d.np * sizeof(NormSlot*), cudaMemcpyHostToDevice, s0));
   XDesc xd{};
   xd.slots = reinterpret_cast<const Slot*>(arena + lay.slots);
   xd.peer_slots = d_peer_slots;
   xd.np = d.np;
   xd.rank = d.rank;
   xd.rescale = d.rescale;
+  xd.abort = abort_flag;
   for (int q = 0; q < kStar; ++q) xd.owner[q] = static_cast<signed char>(star_owner[q]);
   xd.mine = star_mine;
+  if (fused) {
+    for (int f = 0; f < 6; ++f) {
+      const int nb = rank_at[f];
+      if (nb < 0) continue;  // a wall
+      const host::Extent& ne = ext[nb];
+      const std::array<int, 3> nn{ne.size(0), ne.size(1), ne.size(2)};
+      const BlockSpan sp_nb = block_span(nn, host::neighbors(dims, nb), d.strategy, d.np);
+      FaceSend& fsd = xd.face[f];
+      for (int q = 0; q < 2; ++q)
+        fsd.base[q] = reinterpret_cast<double*>(peer_arena[nb] + sp_nb.state_off + q * sp_nb.state_bytes);
+      fsd.fstride = sp_nb.g.fstride;
+      fsd.pitch = sp_nb.g.pitch;
+      fsd.ypitch = sp_nb.g.ypitch;
+      fsd.off = sp_nb.g.off;
+      const int ax = f >> 1;
+      fsd.shift = (f & 1) ? -n[ax] : nn[ax];  // our halo layers -> the neighbour's ghost layers
+      fsd.dq = 1;
+      for (const auto& e : plan)  // the plan's u..T depth on this face (exchange parity of the ghost storage)
+        if (e.face == f)
+          for (int v = 0; v < e.nvars; ++v)
+            if (e.var[v] != 0) fsd.dq = std::max(fsd.dq, e.depth[v]);
+      xd.xmask |= 1 << f;
+    }
+  }
   xd.sp = sp;
   xd.bf = bf;
   xd.dx = dx;
@@ -909,6 +1068,7 @@ void Block::ensure_ready() {
 
 void Block::prologue() {
   ++gen;
+  chk_count = 0;
   Acc z[2] = {};
   z[0].err = z[1].err = ~0ull;
   CAV_CUDA(cudaMemcpyAsync(acc, z, sizeof z, cudaMemcpyHostToDevice, s0));
@@ -929,6 +1089,43 @@ void Block::prologue() {
                                    d.rescale, err, cx, cy, cz);
     CAV_CUDA(cudaGetLastError());
   } else {
+    if (fused) {
+      // 1. tell every joined neighbour our state is in place (it may write
+      //    halos into it from now on), 2. wait until theirs are, 3. send the
+      //    initial state's halos; push(0) below then releases them with the
+      //    scalars (every later state's halos ride on the step kernel)
+      PeerWords pw{};
+      for (int f = 0; f < 6; ++f)
+        if (rank_at[f] >= 0)
+          pw.w[pw.n++] = reinterpret_cast<unsigned long long*>(peer_arena[rank_at[f]]) + kReadyWord + (f ^ 1);
+      k_signal<<<1, 32, 0, s0>>>(pw, base());
+      CAV_CUDA(cudaGetLastError());
+      prog->ready.store(base(), std::memory_order_release);
+      std::vector<std::pair<const unsigned long long*, unsigned long long>> w;
+      for (int f = 0; f < 6; ++f)
+        if (rank_at[f] >= 0) {
+          wait_host(rank_at[f], &HostProgress::ready, base(), 1);
+          w.emplace_back(reinterpret_cast<unsigned long long*>(arena) + kReadyWord + f, base());
+        }
+      stream_wait_geq(s0, w, wait_flags);
+      for (int f = 0; f < 6; ++f) {
+        if (rank_at[f] < 0) continue;
+        const int ax = f >> 1;
+        for (int layer = 0; layer < 2; ++layer) {  // layer 0: p, u, v, w, T; layer 1: p (+ u..T at depth 2)
+          cav_box b{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
+          b.lo[ax] = (f & 1) ? n[ax] + 1 - layer : 2 + layer;
+          b.hi[ax] = b.lo[ax] + 1;
+          int dq = 1;
+          for (const auto& e : plan)
+            if (e.face == f)
+              for (int v = 0; v < e.nvars; ++v)
+                if (e.var[v] != 0) dq = std::max(dq, e.depth[v]);
+          const int bits = layer == 0 ? 3 : (dq == 2 ? 3 : 1);
+          k_face_send<<<296, 256, 0, s0>>>(state[cur], g, d_xd, cur, b, bits << (2 * f));
+          CAV_CUDA(cudaGetLastError());
+        }
+      }
+    }
     launch_push(0);  // iteration 0's maxima (the scan) and the initial state's centre star
   }
   primed = true;
@@ -963,7 +1160,7 @@ long long Block::launch_step(int part, long long it, bool check, unsigned long l
   a.sp = sp;
   a.bf = bf;
   a.work = counters + kCtrWork;
-  a.stop = d.np > 1 ? abort_flag : stop_flag;
+  a.stop = stop_flag ? stop_flag : (d.np > 1 ? abort_flag : nullptr);
   a.box = cav_box{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
   a.sc = sc + (it & 1);
   a.acc = acc + (it & 1);
@@ -982,7 +1179,7 @@ long long Block::launch_step(int part, long long it, bool check, unsigned long l
   // chunks below trim the end (measured at 256^3: 48 best of 24..96, +0.6%
   // over 32). Small boxes get shorter chunks so that there are items for
   // every CTA (a 32^3 block has 4 tiles: 48-plane items would leave 292 CTAs idle).
-  const bool split = d.np > 1 && d.overlap;
+  const bool split = d.np > 1 && d.overlap && !fused;
   a.zl = split ? zsh[0] : 0;
   a.zh = split ? zsh[1] : 0;
   a.mlo = a.box.lo[2] + 2 * a.zl;
@@ -1046,9 +1243,10 @@ long long Block::launch_step(int part, long long it, bool check, unsigned long l
     a.xpush = push ? 1 : 0;
     a.push_par = static_cast<int>(it & 1);
     a.push_stamp = base() + static_cast<unsigned long long>(it) + 1;
+    a.out_par = cur ^ 1;
   }
   const int grid = static_cast<int>(std::min<long long>(tma_grid, wanted));
-  tma_launch<TmaV0>(tmap[cur], a, check, ghosts, grid, s0);
+  tma_launch<TmaV0>(tmap[cur], a, check, ghosts, fused && xfold, grid, s0);
   if (push) prog->push.store(base() + static_cast<unsigned long long>(it), std::memory_order_release);
   return wanted;
 }
@@ -1059,7 +1257,8 @@ void Block::launch_ghosts() {
   if (step_wrote_ghosts) {
     if (!(walls[2] || walls[3] || walls[4] || walls[5])) return;
     const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
-    k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo, d.np > 1 ? abort_flag : stop_flag);
+    k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo,
+                                                stop_flag ? stop_flag : (d.np > 1 ? abort_flag : nullptr));
     CAV_CUDA(cudaGetLastError());
   } else {
     double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
@@ -1081,6 +1280,23 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
     cur ^= 1;
     return;
   }
+  if (fused) {
+    // halos travelled inside every rank's previous step (their last CTA
+    // released the scalar stamps after them), so the scalar wait covers both
+    mark(0, s0);
+    wait_scalars(it);
+    mark(1, s0);
+    mark(2, s0);
+    launch_step(0, it, check, dig, true, true, true, false);
+    mark(3, s0);
+    mark(4, s0);
+    mark(5, s0);
+    if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, stop_flag ? stop_flag : abort_flag, s0);
+    launch_ghosts();
+    mark(6, s0);
+    cur ^= 1;
+    return;
+  }
   XArgs x{};
   x.state = state[cur];
   x.g = g;
@@ -1088,6 +1304,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
   x.val = base() + static_cast<unsigned long long>(it);
   x.corrupt = d.corrupt_exchange;
   x.abort = abort_flag;
+  x.stop = stop_flag ? stop_flag : abort_flag;
   long long maxs = 0;
   for (const auto& e : plan) maxs = std::max(maxs, e.scalars);
   const dim3 xgrid(static_cast<unsigned>((maxs + kXThreads * kXItems - 1) / (kXThreads * kXItems)),
@@ -1142,7 +1359,7 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
     mark(4, s0);
     mark(5, s0);
   }
-  if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, abort_flag, s0);
+  if (step_used_scratch) launch_norm_runs(rscratch, g, ib, dig, err, it, d.rank, stop_flag ? stop_flag : abort_flag, s0);
   launch_ghosts();
   mark(6, s0);
   cur ^= 1;
@@ -1231,16 +1448,18 @@ void Block::on_timeout(long long hint) {
     out += (out.empty() ? "" : ", ");
     out += "(src=" + std::to_string(src) + ", tag=" + std::to_string(tag) + ")";
   };
-  for (size_t m = 0; m < plan.size(); ++m)
-    if (flags[m] < want) add(plan[m].neighbor, plan[m].recv_tag);
+  auto stamp_missing = [&](int r) { return slots[r * 2 + ((stuck - 1) & 1)].stamp < want; };
+  for (size_t m = 0; m < plan.size(); ++m)  // fused halos arrive with the neighbour's scalars
+    if (fused ? stamp_missing(plan[m].neighbor) : flags[m] < want) add(plan[m].neighbor, plan[m].recv_tag);
   for (int r = 0; r < d.np; ++r)
     if (r != d.rank && slots[r * 2 + ((stuck - 1) & 1)].stamp < want) add(r, 1001);  // kReduceTag
   // abort: later kernels return at once; release every wait so the streams drain
   const int one = 1;
   CAV_CUDA(cudaMemcpyAsync(abort_flag, &one, sizeof one, cudaMemcpyHostToDevice, saux));
+  if (stop_flag) CAV_CUDA(cudaMemcpyAsync(&conv->stop, &one, sizeof one, cudaMemcpyHostToDevice, saux));
   const unsigned long long big = ~0ull >> 1;
-  std::vector<unsigned long long> fl(plan.size(), big);
-  if (!fl.empty()) CAV_CUDA(cudaMemcpyAsync(arena, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, saux));
+  std::vector<unsigned long long> fl(64, big);  // plan-entry flags and the ready words
+  CAV_CUDA(cudaMemcpyAsync(arena, fl.data(), fl.size() * 8, cudaMemcpyHostToDevice, saux));
   for (auto& s : slots) s.stamp = big;
   for (int r = 0; r < d.np; ++r)
     for (int p = 0; p < 2; ++p)
@@ -1442,9 +1661,9 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     if (nchk) CAV_CUDA(cudaMemsetAsync(b.digits, 0, nchk * kNormWords * sizeof(unsigned long long), b.s0));
     if (!b.primed) b.prologue();
     if (mark) b.host_marks[2] = host_now();
-    // device convergence: single-rank blocks only (other ranks' norm
-    // partials would have to be merged first; those runs fold on the host)
-    const bool dconv = io->device_conv && io->want_norms && b.d.np == 1;
+    // device convergence (many ranks: every rank's digits merged on every
+    // device after each check, see k_push_norms / k_conv_check)
+    const bool dconv = io->device_conv && io->want_norms;
     io->device_conv = dconv ? 1 : 0;
     const int cur0 = b.cur;
     if (dconv) {
@@ -1469,7 +1688,26 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
       ci += chk;
       b.iteration(it, chk, dig, nullptr);
       if (dconv && chk) {
-        k_conv_check<<<1, 32, 0, b.s0>>>(dig, b.conv, it, io->conv_tol, nglobal);
+        const NormSlot* merge = nullptr;
+        int par = 0;
+        if (b.d.np > 1) {  // every rank's digits of this check into every rank's norm slot, then wait for all
+          const long long c = b.chk_count++;
+          par = static_cast<int>(c & 1);
+          const unsigned long long stamp = b.base() + static_cast<unsigned long long>(c) + 1;
+          k_push_norms<<<std::min(b.d.np, 8), 256, 0, b.s0>>>(dig, b.d_peer_norms, b.d.np, b.d.rank, par, stamp,
+                                                               b.stop_flag);
+          CAV_CUDA(cudaGetLastError());
+          b.prog->norm.store(b.base() + static_cast<unsigned long long>(c), std::memory_order_release);
+          merge = reinterpret_cast<const NormSlot*>(b.arena + b.lay.norms);
+          std::vector<std::pair<const unsigned long long*, unsigned long long>> w;
+          for (int r = 0; r < b.d.np; ++r) {
+            b.wait_host(r, &HostProgress::norm, b.base() + static_cast<unsigned long long>(c), it);
+            w.emplace_back(&merge[r * 2 + par].stamp, stamp);
+          }
+          stream_wait_geq(b.s0, w, b.wait_flags);
+        }
+        k_conv_check<<<1, 128, 0, b.s0>>>(dig, b.conv, it, io->conv_tol, nglobal, merge, b.d.np, par,
+                                          b.base() + static_cast<unsigned long long>(b.chk_count), b.abort_flag);
         CAV_CUDA(cudaGetLastError());
       }
       if (mark && it == 1) b.host_marks[3] = host_now();
@@ -1553,7 +1791,8 @@ int cav_block_launches_per_iteration(cav_block* bh, int check) {
   // step (two launches when overlapping), [ghosts after a stored-ghost step], [k_norm_runs]
   int n = (b.d.np > 1 && b.d.overlap ? 2 : 1) + (b.ghosts && (yz || !b.ghost_writes) && walls ? 1 : 0) +
           (check && b.ghosts ? 1 : 0);
-  if (b.d.np > 1) n += b.plan.empty() ? 0 : 2;  // pack, unpack (fold and push ride on the step kernel)
+  if (b.fused) n = 1 + (b.ghosts && (yz || !b.ghost_writes) && walls ? 1 : 0) + (check && b.ghosts ? 1 : 0);
+  else if (b.d.np > 1) n += b.plan.empty() ? 0 : 2;  // pack, unpack (fold and push ride on the step kernel)
   return n;
 }
 

@@ -184,11 +184,12 @@ void rank_main(Shared& sh, int rank) {
   cav_run_io io{};
   double seconds = 0.0;
   long long it = 1;
-  // One rank: the convergence rule runs on the device after every check, so
-  // a segment can span many checks without a host round trip (the segment
-  // stops where the run converged). Several ranks: one check per segment,
-  // folded here across ranks.
-  bool dconv = !fixed && sh.np == 1;  // confirmed by the block after the first (1-iteration) segment
+  // The convergence rule runs on the device after every check (several
+  // ranks: on every rank, over every rank's exact digits, pushed GPU to GPU),
+  // so a segment can span many checks without a host round trip; the segment
+  // stops where the run converged. The host folds the segment's partials for
+  // the history afterwards (the same digits, the same decision).
+  bool dconv = !fixed;  // confirmed by the block after the first (1-iteration) segment
   double conv_peaks[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   while (it <= target) {
     long long end = target;

@@ -171,12 +171,34 @@ struct StarCells {       // this rank's share of the centre star
   long long idx[kStar];  // storage index within the field
 };
 
+// Halo of one joined face, sent by the step kernel itself (X): every
+// output cell within the face's send layers (p: 2, u,v,w,T: 1 — what the
+// neighbour's stencils read; exchange_begin/copy_box_to's face_interior_box,
+// src/exchange.cpp:115-145, src/slab.cpp:33-52) is stored straight into the
+// neighbour's state — the ghost cell of the same global position — over
+// NVLink / peer memory. base[s] is the neighbour's state s (ranks swap
+// states in lockstep); shift maps our coordinate along the face axis to the
+// neighbour's.
+struct FaceSend {
+  double* base[2];
+  long long fstride;
+  int pitch, ypitch, off, shift;
+  int dq;  // u, v, w, T layers the plan sends on this face (1: V3 / V2 i-faces, else 2); p: always 2
+};
+
+// Halo bits of a cell in layer L (1 = next to the face, 2 = behind it, 0 =
+// neither) of a face whose u..T depth is dq: bit 0 p, bit 1 u, v, w, T.
+__device__ __forceinline__ int halo_bits(int L, int dq) { return L == 1 ? 3 : (L == 2 ? (dq == 2 ? 3 : 1) : 0); }
+
 // Per-block constants of the cross-rank scalars, in device memory (written
 // once when the block connects), so the kernels pass one pointer.
 struct XDesc {
+  FaceSend face[6];
+  int xmask;                // joined faces whose halos the step sends (X)
   const Slot* slots;        // this rank's arena: Slot[np][2]
   Slot* const* peer_slots;  // every rank's Slot array
   int np, rank, rescale;
+  const int* abort;          // set by a transport timeout: stop waiting
   signed char owner[kStar];  // rank holding each star value
   StarCells mine;
   cav_stencil_params sp;
@@ -190,12 +212,21 @@ struct XDesc {
 // before the launch, so plain L2 loads see the pushed values (a stamp below
 // `stamp` only remains after an abort released the wait: skipped).
 __device__ __noinline__ void fold_scalars_warp(const XDesc* x, int par, unsigned long long stamp, double* sstar,
-                                               double* out_dt, double* out_pcs, unsigned long long* out_err) {
+                                               double* out_dt, double* out_pcs, unsigned long long* out_err,
+                                               uint64_t* gate) {
   const int lane = threadIdx.x & 31;
   unsigned long long d0 = 0, d1 = 0, d2 = 0, e = ~0ull;
   for (int r = lane; r < x->np; r += 32) {
     const Slot* s = x->slots + (r * 2 + par);
-    if (__ldcg(&s->stamp) < stamp) continue;
+    // the stream waited for the stamp; the acquire orders the reads below after
+    // the pusher's release (a lagging view waits here; an abort releases it)
+    bool ok = true;
+    while (ld_acquire_sys(&s->stamp) < stamp)
+      if (*reinterpret_cast<const volatile int*>(x->abort)) {
+        ok = false;
+        break;
+      }
+    if (!ok) continue;
     d0 = max(d0, __ldcg(&s->d[0]));
     d1 = max(d1, __ldcg(&s->d[1]));
     d2 = max(d2, __ldcg(&s->d[2]));
@@ -209,6 +240,7 @@ __device__ __noinline__ void fold_scalars_warp(const XDesc* x, int par, unsigned
     e = min(e, __shfl_xor_sync(0xffffffffu, e, o));
   }
   __syncwarp();
+  if (gate && lane == 0) tma::mbar_arrive(gate);  // every stamp acquired: the issuer may load this state
   if (lane != 0) return;
   const unsigned long long dm[3] = {d0, d1, d2};
   cav_fluid_params fl{};
@@ -271,6 +303,28 @@ __device__ __noinline__ void push_scalars_warp(const XDesc* x, int par, unsigned
   }
 }
 
+// One output cell's halo contributions (X): m holds two bits per face (2f:
+// within the face's two p layers, 2f+1: within its u..T layer).
+__device__ __noinline__ void send_cell(const XDesc* x, int par, int i, int j, int k, int m, double p, double u,
+                                       double v, double w, double t) {
+  for (int f = 0; f < 6; ++f) {
+    const int bits = (m >> (2 * f)) & 3;
+    if (!bits) continue;
+    const FaceSend fs = x->face[f];
+    int c[3] = {i, j, k};
+    c[f >> 1] += fs.shift;
+    const long long q = fs.off + c[0] + static_cast<long long>(fs.pitch) * (c[1] + static_cast<long long>(fs.ypitch) * c[2]);
+    double* b = fs.base[par];
+    b[q] = p;
+    if (bits & 2) {
+      b[q + fs.fstride] = u;
+      b[q + 2 * fs.fstride] = v;
+      b[q + 3 * fs.fstride] = w;
+      b[q + 4 * fs.fstride] = t;
+    }
+  }
+}
+
 struct TmaStepArgs {
   double* out;
   Geo g;
@@ -318,6 +372,7 @@ struct TmaStepArgs {
   // the iteration's last launch pushes (xpush) and resets acc_next
   const XDesc* xd;
   int xfold, write_sc, xpush;
+  int out_par;  // index of the output state (cur ^ 1): the neighbours' state the halos go to (X)
   int fold_par, push_par;
   unsigned long long fold_stamp, push_stamp;
   // G norm iterations: the residuals go to this scratch state (same layout)
@@ -553,7 +608,7 @@ __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* d
 // accessor everywhere. Without G they are formed in registers (x/y:
 // SmemAcc<.., true>, z: the p window rules below); the three accessor
 // instances cost 16% at 256^3 even though few warps take the wall paths.
-template <class Cfg, bool NORMS, bool G>
+template <class Cfg, bool NORMS, bool G, bool X>
 __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     k_step_tma(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
                const TmaStepArgs a) {
@@ -566,14 +621,24 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   long long* sitem = reinterpret_cast<long long*>(empty + R);  // item of each slot's entry (-1 = end)
   unsigned long long* sdig = reinterpret_cast<unsigned long long*>(sitem + R);
 
-  // the run converged at an earlier check (device decision): march no further
-  if (a.stop && *reinterpret_cast<const volatile int*>(a.stop)) return;
+  // the run converged at an earlier check (device decision): march no
+  // further; many ranks still advance the scalar stamps their peers wait for
+  if (a.stop && *reinterpret_cast<const volatile int*>(a.stop)) {
+    if (a.xpush && blockIdx.x == 0 && threadIdx.x < 32)
+      for (int r = threadIdx.x; r < a.xd->np; r += 32)
+        st_release_sys(&(a.xd->peer_slots[r] + (a.xd->rank * 2 + a.push_par))->stamp, a.push_stamp);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // X: the issuer's first TMA waits until warp 0's fold has acquired every
+  // rank's stamp (the peers' halo stores into this state precede them)
+  __shared__ uint64_t sgate;
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {
       tma::mbar_init(&full[s], 1);
       tma::mbar_init(&empty[s], C);
     }
+    if (X) tma::mbar_init(&sgate, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (NORMS)
@@ -585,6 +650,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
     if (lane != 0) return;
+    if (X && a.xfold) {
+      tma::mbar_wait(&sgate, 0);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy acquire -> TMA reads
+    }
     Issuer iq{};
     iq.item = blockIdx.x;
     while (iq.item < total && !item_wanted(a, iq.item)) iq.item = gridDim.x + atomicAdd(a.work, 1u);
@@ -608,7 +677,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     __shared__ double sfold[2], sstar[kStar];
     if (warp == 0) {
       unsigned long long e;
-      fold_scalars_warp(a.xd, a.fold_par, a.fold_stamp, sstar, &sfold[0], &sfold[1], &e);
+      fold_scalars_warp(a.xd, a.fold_par, a.fold_stamp, sstar, &sfold[0], &sfold[1], &e, X ? &sgate : nullptr);
       if (lane == 0 && a.write_sc && blockIdx.x == 0) {
         a.sc->dt = sfold[0];
         a.sc->pc = 0.0;
@@ -652,6 +721,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // tiles) compute on whatever the slot holds there, without storing or reducing, so
   // the cell is not under a branch (1.4% faster at 256^3).
   bool live = true;
+  int smask_xy = 0;       // X: this column's x/y halo layer bits (send_cell)
+  const int xmask = X ? a.xd->xmask : 0;  // X: joined faces
+  int ci = 0, cj = 0;     // X: this thread's column
+  bool sxy_warp = false;  // X: some lane of this warp has x/y halo cells
   auto wait_planes = [&](int count, int* sl) {
     for (int q = 0; q < count; ++q) {
       sl[q] = sw;
@@ -749,6 +822,18 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         __stcs(op + 4 * fs + sg, 2.0 * (h ? a.walls.t_cold : a.walls.t_hot) - qtn);
       }
     }
+    if (X) {  // halo cells of joined faces: straight into the neighbours' states
+      const int xm = xmask;
+      const bool zs = ((xm & 16) && kk <= 3) || ((xm & 32) && kk >= g.nz);
+      if (sxy_warp || zs) {
+        int m = smask_xy;
+        if (zs && live) {
+          if (xm & 16) m |= halo_bits(kk == 2 ? 1 : (kk == 3 ? 2 : 0), a.xd->face[4].dq) << 8;
+          if (xm & 32) m |= halo_bits(kk == g.nz + 1 ? 1 : (kk == g.nz ? 2 : 0), a.xd->face[5].dq) << 10;
+        }
+        if (m) send_cell(a.xd, a.out_par, ci, cj, kk, m, qpn, qun, qvn, qwn, qtn);
+      }
+    }
     if (!G || live) {
       const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, a.bf);
       m0 = dmax_d(m0, d.du);
@@ -789,6 +874,18 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
     live = active;
+    if (X) {  // this column's x/y halo layers (fused send)
+      const int xm = xmask;
+      int mm = 0;
+      if (xm & 1) mm |= halo_bits(i == 2 ? 1 : (i == 3 ? 2 : 0), a.xd->face[0].dq);
+      if (xm & 2) mm |= halo_bits(i == g.nx + 1 ? 1 : (i == g.nx ? 2 : 0), a.xd->face[1].dq) << 2;
+      if (xm & 4) mm |= halo_bits(j == 2 ? 1 : (j == 3 ? 2 : 0), a.xd->face[2].dq) << 4;
+      if (xm & 8) mm |= halo_bits(j == g.ny + 1 ? 1 : (j == g.ny ? 2 : 0), a.xd->face[3].dq) << 6;
+      smask_xy = active ? mm : 0;
+      ci = i;
+      cj = j;
+      sxy_warp = __any_sync(0xffffffffu, smask_xy != 0);
+    }
     // x/y walls next to this thread's column: register ghosts (SmemAcc<.., true>)
     if (G && a.gw) {  // wfl (G): 1 = i == 2 at the low x wall, 2 = i == nx+1 at the high one, 4 = in this warp
       const int xl = a.walls.wall[0] && i == 2, xh = a.walls.wall[1] && i == g.nx + 1;
@@ -872,6 +969,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       const unsigned long long m = warp_max_u64(lmax[v]);
       if (lane == 0 && m) atomicMax(&sdig[5 * kDigits + v], m);
     }
+  if (X) __threadfence_system();  // this thread's halo stores, before the flag/stamp release of the last CTA
   // consumer-only reductions
   constexpr int NC = 32 * C;
   __shared__ double sred[3][C];
@@ -903,6 +1001,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
     __threadfence();
     last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    if (X && last) __threadfence_system();
     if (last) {  // every CTA has published
       *a.work = 0;
       __threadfence();

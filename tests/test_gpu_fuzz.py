@@ -42,11 +42,14 @@ def draw(seed):
 
 
 @pytest.mark.parametrize("seed", list(range(48)))
-@pytest.mark.parametrize("ghosts", ["auto", "1"])
+@pytest.mark.parametrize("ghosts", ["auto", "1", "slab"])
 def test_random_configuration_matches_oracle(monkeypatch, seed, ghosts):
-    """ghosts "1" forces the stored-wall-ghost step on every single-rank
-    draw (by default it starts at 3e6 cells, above these grids)."""
+    """ghosts "1" forces the stored-wall-ghost step on every draw (by default
+    it starts at 3e6 cells per block, above these grids); "slab" runs the
+    multi-rank draws through the pack/unpack slab exchange instead of the
+    step kernel's fused halo stores."""
     monkeypatch.setenv("CAV_STORED_GHOSTS", "1" if ghosts == "1" else "-1")
+    monkeypatch.setenv("CAV_FUSED_HALO", "0" if ghosts == "slab" else "1")
     kw = draw(seed)
     r = capi.run_case(capi.default_config(**kw), collect_fields=True, collect_history=True)
     serial = {k: v for k, v in kw.items() if k not in ("np", "mode", "strategy", "overlap")}

@@ -55,9 +55,14 @@ def test_timeout_names_waiting_rank_and_stuck_sources():
         b.close()
 
 
-def test_timeout_at_a_later_iteration():
+@pytest.mark.parametrize("fused", [True, False])
+def test_timeout_at_a_later_iteration(monkeypatch, fused):
     """A peer that stops after some iterations: the waiting rank names it at
-    the first iteration it cannot complete."""
+    the first iteration it cannot complete. With fused halos (default) the
+    peer's step n already sent S_n's halos, so iteration 5 completes and the
+    wait for its scalars of iteration 5 times out at 6; the slab exchange
+    (CAV_FUSED_HALO=0) sends S_4's halos at iteration 5, like the reference."""
+    monkeypatch.setenv("CAV_FUSED_HALO", "1" if fused else "0")
     grid, dims = (20, 12, 10), (2, 1, 1)
     a, b = (capi.Block(r, 2, grid, dims, strategy="v3", overlap=True, timeout_ms=300.0) for r in range(2))
     a.connect(1, ptr=b.arena())
@@ -73,7 +78,8 @@ def test_timeout_at_a_later_iteration():
     # rank 1 marched iterations 1..4: its scalars reach rank 0's fold of
     # iteration 5, its halo of iteration 5 never comes
     entry = capi.build_plan(a.n, capi.neighbors(dims, 0), "v3")[0]
-    assert str(ex.value).startswith("rank 0: receive timed out at iteration 5; outstanding: ")
+    stuck = 6 if fused else 5
+    assert str(ex.value).startswith(f"rank 0: receive timed out at iteration {stuck}; outstanding: ")
     assert f"(src=1, tag={entry['recv_tag']})" in str(ex.value)
     a.close()
     b.close()
@@ -187,3 +193,28 @@ print("ONE-QUEUE-OK")
     env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="1")
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
     assert p.returncode == 0 and "ONE-QUEUE-OK" in p.stdout, p.stdout + p.stderr
+
+
+_SOLVE_REF = {}
+
+
+@pytest.mark.parametrize("kw", [dict(np=2, mode="1d-k", strategy="v3", overlap=1),
+                                dict(np=4, mode="2d", strategy="v1", overlap=0),
+                                dict(np=8, mode="3d", strategy="v3", overlap=1)])
+def test_multi_rank_device_converged_solve(kw):
+    """`cavity solve` on several ranks decided on the devices: after every
+    check each rank pushes its exact norm digits to every rank, every rank
+    merges them and applies the rule of src/runner.cpp:210-220 (no host round
+    trip per check). Same converged iteration, history and fields as the
+    oracle, and one exchange per marched iteration in every rank's ledger."""
+    cfg = capi.default_config(grid=(32, 32, 32), steps=-1)
+    if "o" not in _SOLVE_REF:
+        _SOLVE_REF["o"] = Oracle.run_case(cfg, collect_fields=True, collect_history=True)
+    o = _SOLVE_REF["o"]
+    r = capi.run_case(capi.default_config(grid=(32, 32, 32), steps=-1, **kw), collect_fields=True,
+                      collect_history=True)
+    assert r.converged and o["converged"] and r.steps_marched == o["steps_marched"]
+    assert list(r.history_iter) == list(o["history_iter"])
+    np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
+    np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
+    assert all(l["exchanges"] == r.steps_marched for l in r.ledgers)
