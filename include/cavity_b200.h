@@ -267,9 +267,11 @@ typedef struct {
 
 int cav_block_create(const cav_block_desc* desc, cav_block** out);
 int cav_block_destroy(cav_block* b);
-/* Exchange arena (receive slabs, flags, scalar slots) of this block: raw
- * device pointer for in-process peers, CUDA IPC handle (64 bytes) for peers
- * in other processes. */
+/* This block's device memory as peers see it: ONE allocation holding the
+ * exchange arena (flags, scalar and norm slots, receive slabs) followed by the
+ * two states the neighbours' step kernels store halos into (fused halos).
+ * Raw device pointer for in-process peers, CUDA IPC handle (64 bytes) for
+ * peers in other processes; bytes_out is the arena part. */
 int cav_block_arena(cav_block* b, void** dev_ptr_out, size_t* bytes_out);
 int cav_block_arena_ipc(cav_block* b, unsigned char handle_out[64]);
 /* Connect rank r's arena: exactly one of dev_ptr / ipc_handle is non-NULL. */

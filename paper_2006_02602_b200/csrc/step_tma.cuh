@@ -305,15 +305,15 @@ __device__ __noinline__ void push_scalars_warp(const XDesc* x, int par, unsigned
 
 // One output cell's halo contributions (X): m holds two bits per face (2f:
 // within the face's two p layers, 2f+1: within its u..T layer).
-__device__ __noinline__ void send_cell(const XDesc* x, int par, int i, int j, int k, int m, double p, double u,
+__device__ __forceinline__ void send_cell(const XDesc* x, int par, int i, int j, int k, int m, double p, double u,
                                        double v, double w, double t) {
   for (int f = 0; f < 6; ++f) {
     const int bits = (m >> (2 * f)) & 3;
     if (!bits) continue;
-    const FaceSend fs = x->face[f];
-    int c[3] = {i, j, k};
-    c[f >> 1] += fs.shift;
-    const long long q = fs.off + c[0] + static_cast<long long>(fs.pitch) * (c[1] + static_cast<long long>(fs.ypitch) * c[2]);
+    const FaceSend& fs = x->face[f];
+    const int ax = f >> 1, sh = fs.shift;  // no indexed local array: selects keep it in registers
+    const int c0 = i + (ax == 0 ? sh : 0), c1 = j + (ax == 1 ? sh : 0), c2 = k + (ax == 2 ? sh : 0);
+    const long long q = fs.off + c0 + static_cast<long long>(fs.pitch) * (c1 + static_cast<long long>(fs.ypitch) * c2);
     double* b = fs.base[par];
     b[q] = p;
     if (bits & 2) {
@@ -721,10 +721,10 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
   // tiles) compute on whatever the slot holds there, without storing or reducing, so
   // the cell is not under a branch (1.4% faster at 256^3).
   bool live = true;
-  int smask_xy = 0;       // X: this column's x/y halo layer bits (send_cell)
-  const int xmask = X ? a.xd->xmask : 0;  // X: joined faces
-  int ci = 0, cj = 0;     // X: this thread's column
-  bool sxy_warp = false;  // X: some lane of this warp has x/y halo cells
+  // X, per item (two registers on the hot path): xs = this lane's x/y halo
+  // bits (0-7) | some lane of the warp has x/y halo cells (8) | the item
+  // reaches a joined z face's halo planes (9); xij = i | j << 16
+  int xs = 0, xij = 0;
   auto wait_planes = [&](int count, int* sl) {
     for (int q = 0; q < count; ++q) {
       sl[q] = sw;
@@ -822,17 +822,14 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         __stcs(op + 4 * fs + sg, 2.0 * (h ? a.walls.t_cold : a.walls.t_hot) - qtn);
       }
     }
-    if (X) {  // halo cells of joined faces: straight into the neighbours' states
-      const int xm = xmask;
-      const bool zs = ((xm & 16) && kk <= 3) || ((xm & 32) && kk >= g.nz);
-      if (sxy_warp || zs) {
-        int m = smask_xy;
-        if (zs && live) {
-          if (xm & 16) m |= halo_bits(kk == 2 ? 1 : (kk == 3 ? 2 : 0), a.xd->face[4].dq) << 8;
-          if (xm & 32) m |= halo_bits(kk == g.nz + 1 ? 1 : (kk == g.nz ? 2 : 0), a.xd->face[5].dq) << 10;
-        }
-        if (m) send_cell(a.xd, a.out_par, ci, cj, kk, m, qpn, qun, qvn, qwn, qtn);
+    if (X && (xs & 0x300)) {  // halo cells of joined faces: straight into the neighbours' states
+      int m = xs & 0xFF;
+      if ((xs & 0x200) && live) {
+        const int xm = a.xd->xmask;
+        if (xm & 16) m |= halo_bits(kk == 2 ? 1 : (kk == 3 ? 2 : 0), a.xd->face[4].dq) << 8;
+        if (xm & 32) m |= halo_bits(kk == g.nz + 1 ? 1 : (kk == g.nz ? 2 : 0), a.xd->face[5].dq) << 10;
       }
+      if (m) send_cell(a.xd, a.out_par, xij & 0xFFFF, xij >> 16, kk, m, qpn, qun, qvn, qwn, qtn);
     }
     if (!G || live) {
       const Denoms d = cfl_denoms(qun, qvn, qwn, u_ref, a.bf);
@@ -875,16 +872,16 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
     live = active;
     if (X) {  // this column's x/y halo layers (fused send)
-      const int xm = xmask;
+      const int xm = a.xd->xmask;
       int mm = 0;
       if (xm & 1) mm |= halo_bits(i == 2 ? 1 : (i == 3 ? 2 : 0), a.xd->face[0].dq);
       if (xm & 2) mm |= halo_bits(i == g.nx + 1 ? 1 : (i == g.nx ? 2 : 0), a.xd->face[1].dq) << 2;
       if (xm & 4) mm |= halo_bits(j == 2 ? 1 : (j == 3 ? 2 : 0), a.xd->face[2].dq) << 4;
       if (xm & 8) mm |= halo_bits(j == g.ny + 1 ? 1 : (j == g.ny ? 2 : 0), a.xd->face[3].dq) << 6;
-      smask_xy = active ? mm : 0;
-      ci = i;
-      cj = j;
-      sxy_warp = __any_sync(0xffffffffu, smask_xy != 0);
+      mm = active ? mm : 0;
+      const bool zitem = ((xm & 16) && it.kb <= 3) || ((xm & 32) && it.ke > g.nz);
+      xs = mm | (__any_sync(0xffffffffu, mm != 0) ? 0x100 : 0) | (zitem ? 0x200 : 0);
+      xij = i | (j << 16);
     }
     // x/y walls next to this thread's column: register ghosts (SmemAcc<.., true>)
     if (G && a.gw) {  // wfl (G): 1 = i == 2 at the low x wall, 2 = i == nx+1 at the high one, 4 = in this warp
