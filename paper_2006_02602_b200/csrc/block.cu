@@ -705,6 +705,10 @@ struct Block {
   MsgDesc* d_unpack = nullptr;
   Slot** d_peer_slots = nullptr;
   XDesc* d_xd = nullptr;         // cross-rank scalar constants (step_tma.cuh)
+  long long* iter_dev = nullptr;  // one rank: the iteration the next step computes (TmaStepArgs::n_dev)
+  // one rank: CUDA graphs of two plain iterations, keyed by (cur, it & 1)
+  cudaGraphExec_t gexec[4]{};
+  bool use_graphs = false;
   NormSlot** d_peer_norms = nullptr;  // every rank's NormSlot array (device convergence, np > 1)
   long long chk_count = 0;        // check iterations since the prologue (norm slot parity)
   unsigned long long* digits = nullptr;
@@ -761,6 +765,8 @@ struct Block {
   void launch_push(long long it);
   void launch_ghosts();
   void update_ledger(cav_ledger& l) const;
+  // one rank: iterations it and it+1 (no norms) as one CUDA graph launch
+  void iteration_pair_graph(long long it);
   // np > 1: keeps at most kWindow iterations in flight; polls with the
   // transport timeout (a missing peer raises TransportTimeout, not a hang)
   void window_mark(long long it);
@@ -904,9 +910,12 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
   CAV_CUDA(cudaMalloc(&counters, 64 * sizeof(unsigned)));
   abort_flag = reinterpret_cast<int*>(counters + kCtrAbort);
   CAV_CUDA(cudaMalloc(&conv, sizeof(ConvState)));
+  CAV_CUDA(cudaMemsetAsync(conv, 0, sizeof(ConvState), s0));
   CAV_CUDA(cudaMemsetAsync(counters, 0, 64 * sizeof(unsigned), s0));
   CAV_CUDA(cudaMalloc(&d_peer_slots, d.np * sizeof(Slot*)));
   CAV_CUDA(cudaMalloc(&d_xd, sizeof(XDesc)));
+  CAV_CUDA(cudaMalloc(&iter_dev, sizeof(long long)));
+  use_graphs = d.np == 1 && getenv_int("CAV_GRAPHS", 1) != 0;
   CAV_CUDA(cudaMalloc(&d_peer_norms, d.np * sizeof(NormSlot*)));
   if (!plan.empty()) {
     CAV_CUDA(cudaMalloc(&d_pack, plan.size() * sizeof(MsgDesc)));
@@ -950,6 +959,9 @@ Block::~Block() {
   cudaFree(conv);
   cudaFree(d_peer_slots);
   cudaFree(d_xd);
+  cudaFree(iter_dev);
+  for (auto& ge : gexec)
+    if (ge) cudaGraphExecDestroy(ge);
   cudaFree(d_peer_norms);
   cudaFree(d_pack);
   cudaFree(d_unpack);
@@ -1153,7 +1165,8 @@ long long Block::launch_step(int part, long long it, bool check, unsigned long l
   a.sp = sp;
   a.bf = bf;
   a.work = counters + kCtrWork;
-  a.stop = stop_flag ? stop_flag : (d.np > 1 ? abort_flag : nullptr);
+  a.stop = d.np == 1 ? &conv->stop : (stop_flag ? stop_flag : abort_flag);
+  a.n_dev = d.np == 1 ? iter_dev : nullptr;
   a.box = cav_box{{2, 2, 2}, {n[0] + 2, n[1] + 2, n[2] + 2}};
   a.sc = sc + (it & 1);
   a.acc = acc + (it & 1);
@@ -1251,7 +1264,7 @@ void Block::launch_ghosts() {
     if (!(walls[2] || walls[3] || walls[4] || walls[5])) return;
     const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
     k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo,
-                                                stop_flag ? stop_flag : (d.np > 1 ? abort_flag : nullptr));
+                                                d.np == 1 ? &conv->stop : (stop_flag ? stop_flag : abort_flag));
     CAV_CUDA(cudaGetLastError());
   } else {
     double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
@@ -1356,6 +1369,23 @@ void Block::iteration(long long it, bool check, unsigned long long* dig, IterTim
   launch_ghosts();
   mark(6, s0);
   cur ^= 1;
+}
+
+void Block::iteration_pair_graph(long long it) {
+  const int key = (cur << 1) | static_cast<int>(it & 1);
+  if (!gexec[key]) {  // capture once: the launches' arguments depend only on (cur, it & 1)
+    cudaGraph_t gr = nullptr;
+    CAV_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+    iteration(it, false, nullptr, nullptr);
+    iteration(it + 1, false, nullptr, nullptr);
+    CAV_CUDA(cudaStreamEndCapture(s0, &gr));
+    const cudaError_t e = cudaGraphInstantiate(&gexec[key], gr, 0);
+    cudaGraphDestroy(gr);
+    CAV_CUDA(e);
+    CAV_CUDA(cudaGraphLaunch(gexec[key], s0));
+    return;  // the capture swapped cur twice: unchanged
+  }
+  CAV_CUDA(cudaGraphLaunch(gexec[key], s0));
 }
 
 void Block::update_ledger(cav_ledger& l) const {
@@ -1674,8 +1704,21 @@ int cav_block_run(cav_block* bh, cav_run_io* io) {
     const cav_ledger ledger0 = io->ledger;
     unsigned long long js = b.d.jitter_seed ? b.d.jitter_seed * 0x9E3779B97F4A7C15ull + b.d.rank + 1 : 0;
     long long ci = 0;
+    // one rank: the device iteration counter starts where this call starts
+    if (b.d.np == 1) {
+      CAV_CUDA(cudaMemcpyAsync(b.iter_dev, &first, sizeof first, cudaMemcpyHostToDevice, b.s0));
+      if (!dconv) CAV_CUDA(cudaMemsetAsync(&b.conv->stop, 0, sizeof(int), b.s0));
+    }
     for (long long it = first; it <= last; ++it) {
       const bool chk = is_check(it);
+      // two plain iterations after the warm-up one: one graph launch
+      if (b.use_graphs && it > 1 && it + 1 <= last && !chk && !is_check(it + 1)) {
+        b.iteration_pair_graph(it);
+        b.update_ledger(io->ledger);
+        b.update_ledger(io->ledger);
+        ++it;
+        continue;
+      }
       unsigned long long* dig = chk ? b.digits + ci * kNormWords : nullptr;
       if (chk && io->check_iters) io->check_iters[ci] = it;
       ci += chk;
@@ -1811,6 +1854,11 @@ int cav_block_bench(cav_block* bh, long long n_its, double out[3]) {
       Block::IterTiming t;
       for (auto& e : t.e) e = make_event();
       b.timing.push_back(t);
+    }
+    if (b.d.np == 1) {  // the device iteration counter and a cleared convergence stop
+      const long long first = b.next_n;
+      CAV_CUDA(cudaMemcpyAsync(b.iter_dev, &first, sizeof first, cudaMemcpyHostToDevice, b.s0));
+      CAV_CUDA(cudaMemsetAsync(&b.conv->stop, 0, sizeof(int), b.s0));
     }
     CAV_CUDA(cudaEventRecord(b.ev_a, b.s0));
     for (long long k = 0; k < n_its; ++k) {

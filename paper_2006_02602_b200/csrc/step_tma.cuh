@@ -338,6 +338,9 @@ struct TmaStepArgs {
   unsigned long long* digits;
   int cx, cy, cz;
   long long n;
+  // one rank: the iteration number lives in device memory (advanced by the
+  // last CTA), so a captured CUDA graph of steps can be replayed at any n
+  long long* n_dev;
   int rank;
   int tiles_x, ntiles, chunk, nchunks;
   // chunks [0, nbig) have `chunk` planes from box.lo[2] (the last one may be
@@ -994,8 +997,9 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
       m2 = dmax_d(m2, sred[2][w]);
       mk |= smask[w];
     }
-    acc_publish(a.acc, m0, m1, m2, mk & 0xFF, a.n + 1, a.rank);
-    if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(a.n, a.rank, 0));
+    const long long nn = a.n_dev ? *reinterpret_cast<volatile long long*>(a.n_dev) : a.n;
+    acc_publish(a.acc, m0, m1, m2, mk & 0xFF, nn + 1, a.rank);
+    if (NORMS && (mk >> 8)) atomicMin(&a.acc->err, err_code(nn, a.rank, 0));
     __threadfence();
     last = atomicAdd(a.done, 1u) == gridDim.x - 1;
     if (X && last) __threadfence_system();
@@ -1020,6 +1024,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
         z.err = ~0ull;
         *a.acc_next = z;
       }
+      if (a.n_dev) *a.n_dev = nn + 1;
       *a.done = 0;
     }
   }

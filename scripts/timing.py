@@ -6,6 +6,7 @@
                                       path's extra work: their kernels serialise, so
                                       the sum over ranks is compared with one rank)
   python scripts/timing.py solve      32^3 to convergence
+  python scripts/timing.py runs       per-iteration time of run_case (fixed steps, one rank) by grid size
 
 Every number is device time from cav_block_bench / run_case's own timer.
 """
@@ -50,6 +51,13 @@ def ranks():
             r = capi.run_case(cfg)
             print(f"{grid[0]}^3 np={np_} {mode} overlap={ov}: {r.wall_time_s / r.steps_timed * 1e3:.3f} ms/iteration "
                   f"(all ranks on one GPU)", flush=True)
+
+
+def runs():
+    for n in (32, 64, 128, 256):
+        its = 4000 if n <= 64 else (1000 if n <= 128 else 400)
+        r = capi.run_case(capi.default_config(grid=(n, n, n), steps=its))
+        print(f"n={n}: {r.wall_time_s / r.steps_timed * 1e6:.1f} us/iteration (run_case, {its} steps)", flush=True)
 
 
 def solve():
