@@ -1,4 +1,7 @@
-"""Diagnosis: multi-rank GPU run vs the np=1 GPU run, mismatch locations."""
+"""Multi-rank GPU runs vs the one-rank GPU run of the same case, repeated
+(REPS) to catch rare races: prints how many cells differ and where (per
+variable k/j/i ranges). Env: GRID, NP, MODE, STEPS, REPS, OV, HIST.
+Round 2 used it to find a slab-path unpack that skipped a stale flag."""
 import os, sys
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.join(os.path.dirname(__file__), "..")))
 import numpy as np

@@ -111,3 +111,26 @@ def test_ctypes_prototypes_match_header():
             assert len(at) == n, (name, len(at), n)
             checked += 1
     assert checked >= 10
+
+
+def test_integration_driver_seam_compiles_against_the_reference(tmp_path):
+    """INTEGRATION.md §2's run_case_b200 (the reference-side binding a
+    maintainer adds) compiles against the reference's own headers and ours
+    (g++ -std=c++20 -fsyntax-only); skipped where the reference is absent."""
+    import shutil
+    import subprocess
+    import pytest
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc) or not shutil.which("g++"):
+        pytest.skip("reference headers not available")
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```cpp\n(.*?)```", text, flags=re.S)
+    seam = [b for b in blocks if "run_case_b200" in b]
+    assert seam, "INTEGRATION.md lost its run_case seam"
+    src = tmp_path / "seam.cpp"
+    src.write_text('#include "cavity_b200.h"\n#include <cstring>\n#include <stdexcept>\n#include <vector>\n#include <algorithm>\n'
+                   '#include "cavity/runner.hpp"\n#include "cavity/transport.hpp"\n'
+                   'namespace cavity {\n' + seam[0] + '\n}\n')
+    p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wno-return-type", "-I", ref_inc, "-I",
+                        os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-3000:]
