@@ -218,3 +218,64 @@ def test_multi_rank_device_converged_solve(kw):
     np.testing.assert_array_equal(bits(r.history), bits(o["history"]))
     np.testing.assert_array_equal(bits(r.fields), bits(o["fields"]))
     assert all(l["exchanges"] == r.steps_marched for l in r.ledgers)
+
+
+@pytest.mark.parametrize("dims, strategy, fused", [((2, 1, 1), "v3", "1"), ((1, 2, 2), "baseline", "1"),
+                                                   ((2, 2, 2), "v3", "1"), ((2, 2, 2), "v1", "0")])
+def test_multi_rank_blocks_from_uploaded_state(monkeypatch, dims, strategy, fused):
+    """Several ranks start from an arbitrary uploaded state whose join ghosts
+    are garbage: the exchange must replace them before the first residual
+    (the reference exchanges every iteration before computing it), so the
+    interiors after k steps equal the oracle's serial march of the global
+    state. With fused halos this pins the prologue's initial-halo send
+    (k_face_send) and the in-kernel halo stores from a developed state."""
+    import threading
+    monkeypatch.setenv("CAV_FUSED_HALO", fused)
+    n = (24, 20, 18)
+    gf = O.random_fields(n, 4242, vel=0.03)
+    gf[0] *= 1e-3
+    h = capi.cavity_spacing(n)
+    np_ = dims[0] * dims[1] * dims[2]
+    blocks = [capi.Block(r, np_, n, dims, strategy=strategy) for r in range(np_)]
+    try:
+        for b in blocks:
+            for r in range(np_):
+                if r != b.desc.rank:
+                    b.connect(r, ptr=blocks[r].arena())
+        for b in blocks:
+            lo, m = b.lo, b.n
+            local = gf[:, lo[2]:lo[2] + m[2] + 4, lo[1]:lo[1] + m[1] + 4, lo[0]:lo[0] + m[0] + 4].copy()
+            for a, (l, hi_) in enumerate(((lo[0], lo[0] + m[0]), (lo[1], lo[1] + m[1]), (lo[2], lo[2] + m[2]))):
+                sl = [slice(None)] * 4
+                if l > 0:  # a joined low face: garbage in its ghost layers
+                    sl[3 - a] = slice(0, 2)
+                    local[tuple(sl)] = 7.0e3
+                if hi_ < n[a]:
+                    sl[3 - a] = slice(m[a] + 2, m[a] + 4)
+                    local[tuple(sl)] = -7.0e3
+            b.upload(local)
+        errs = []
+
+        def go(b, k):
+            try:
+                b.run(k)
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+
+        want = gf
+        for k in (3, 4):
+            ts = [threading.Thread(target=go, args=(b, k)) for b in blocks]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            assert not errs, errs
+            want = O.march(want, n, h, capi.fluid_for_rayleigh(1e5), 0.4, k)
+            for b in blocks:
+                lo, m = b.lo, b.n
+                got = b.download()[:, 2:m[2] + 2, 2:m[1] + 2, 2:m[0] + 2]
+                exp = want[:, lo[2] + 2:lo[2] + m[2] + 2, lo[1] + 2:lo[1] + m[1] + 2, lo[0] + 2:lo[0] + m[0] + 2]
+                np.testing.assert_array_equal(bits(got), bits(exp), err_msg=f"rank {b.desc.rank} after {k}")
+    finally:
+        for b in blocks:
+            b.close()
