@@ -2,26 +2,28 @@
 // the B200-native replacement of rank_main's loop body
 // (/root/reference/proj/src/runner.cpp:184-235).
 //
-// Iteration n on rank r. Compute stream s0; the halo exchange runs on s1
-// when overlapping (src/runner.cpp:189-194), else on s0:
-//   pack     k_pack: plan entries of S_{n-1} stored straight into the
-//            neighbours' receive slabs over NVLink/peer memory, one release
-//            flag per entry (exchange_begin, src/exchange.cpp:115-145)
-//   unpack   stream wait on the flags (cuStreamBatchMemOp, no SM occupied),
-//            then k_unpack into the join ghosts (exchange_finish, :147-176)
-//   fold     stream wait on every rank's scalar slot of n-1; every CTA of
-//            the step then folds dt_n (reduce_fixed_order(Min),
-//            src/transport.cpp:23-60, as the exact max rewrite) and pcs_n =
-//            p'(centre) of step n from the gathered centre stencil
-//            (center_pressure_broadcast)
+// Iteration n on rank r (stream s0), fused halos (the default):
+//   fold     stream wait on every rank's scalar slot of n-1; one warp of
+//            every step CTA then acquires the stamps and folds dt_n
+//            (reduce_fixed_order(Min), src/transport.cpp:23-60, as the exact
+//            max rewrite) and pcs_n = p'(centre) of step n from the gathered
+//            centre stencil (center_pressure_broadcast)
 //   step     k_step_tma: BC (register or stored wall ghosts) + residual +
 //            [exact norm digits] + Euler update + eager rescale fl(p'-pcs_n)
-//            + next-step CFL maxima + non-finite flags; internal items, then
-//            (after the halos landed) shell items when overlapping
-//   ghosts   k_ghosts_yz: y/z wall ghosts of S_n (stored-ghost blocks)
+//            + next-step CFL maxima + non-finite flags; every output cell in
+//            a joined face's halo layers is also stored straight into the
+//            neighbour's state over NVLink / peer memory (exchange_begin +
+//            exchange_finish, src/exchange.cpp:115-176, fused into the step)
 //   push     the step's last CTA (k_push before iteration 1): this rank's
 //            maxima, error code and its share of S_n's centre stencil into
-//            every rank's slot, release stamp
+//            every rank's slot, release stamp (after the halo stores)
+//   ghosts   k_ghosts_yz: y/z wall ghosts of S_n (stored-ghost blocks)
+// Slab exchange (CAV_FUSED_HALO=0, the corrupt-exchange hook): k_pack pushes
+// plan entries of S_{n-1} into the neighbours' receive slabs with a release
+// flag per entry; the receiver's stream waits for the flags and k_unpack
+// scatters them into the join ghosts; with overlap this runs on stream s1
+// while the step takes the internal items, the shell items follow
+// (src/runner.cpp:189-194).
 // One rank: the step kernel's last CTA folds dt and pcs itself (no fold or
 // push). Every cross-rank wait is enqueued only after the launch that
 // produces its value has been enqueued (HostProgress below).
