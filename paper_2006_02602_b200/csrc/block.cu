@@ -574,7 +574,16 @@ void tma_attrs() {
 }
 
 template <class Cfg>
+void tma_attrs_full() {
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::Smem)));
+  CAV_CUDA(cudaFuncSetAttribute(k_step_tma<Cfg, false, true, false, true>,
+                                cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+
+template <class Cfg>
 int tma_setup(int device) {
+  tma_attrs_full<Cfg>();
   tma_attrs<Cfg, false, false, false>();
   tma_attrs<Cfg, true, false, false>();
   tma_attrs<Cfg, false, true, false>();
@@ -603,10 +612,16 @@ void tma_launch_x(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool g
 }
 
 template <class Cfg>
-void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, bool send, int grid,
+void tma_launch(const CUtensorMap* m, const TmaStepArgs& a, bool check, bool ghosts, bool send, bool full, int grid,
                 cudaStream_t st) {
-  if (send) tma_launch_x<Cfg, true>(m, a, check, ghosts, grid, st);
-  else tma_launch_x<Cfg, false>(m, a, check, ghosts, grid, st);
+  if (full && ghosts && !check && !send) {  // the production plain step on whole tiles
+    k_step_tma<Cfg, false, true, false, true><<<grid, Cfg::Threads, Cfg::Smem, st>>>(m[0], m[1], a);
+    CAV_CUDA(cudaGetLastError());
+  } else if (send) {
+    tma_launch_x<Cfg, true>(m, a, check, ghosts, grid, st);
+  } else {
+    tma_launch_x<Cfg, false>(m, a, check, ghosts, grid, st);
+  }
 }
 
 // Stream memory operations (driver API): a stream waits for a 64-bit value in
@@ -1254,7 +1269,7 @@ long long Block::launch_step(int part, long long it, bool check, unsigned long l
     a.out_par = cur ^ 1;
   }
   const int grid = static_cast<int>(std::min<long long>(tma_grid, wanted));
-  tma_launch<TmaV0>(tmap[cur], a, check, ghosts, fused && xfold, grid, s0);
+  tma_launch<TmaV0>(tmap[cur], a, check, ghosts, fused && xfold, bw % 32 == 0 && bh % kTY == 0, grid, s0);
   if (push) prog->push.store(base() + static_cast<unsigned long long>(it), std::memory_order_release);
   return wanted;
 }

@@ -611,7 +611,9 @@ __device__ __forceinline__ void digit_run_add(DigitRun& r, unsigned long long* d
 // accessor everywhere. Without G they are formed in registers (x/y:
 // SmemAcc<.., true>, z: the p window rules below); the three accessor
 // instances cost 16% at 256^3 even though few warps take the wall paths.
-template <class Cfg, bool NORMS, bool G, bool X>
+// F: the box is a whole number of tiles (nx % 32 == 0, ny % TY == 0), so
+// every consumer lane is live and the per-cell live tests compile away.
+template <class Cfg, bool NORMS, bool G, bool X, bool F = false>
 __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     k_step_tma(const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapQ,
                const TmaStepArgs a) {
@@ -873,7 +875,7 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
     const int len = it.ke - it.kb;
     const int i = it.ti0 + tx, j = it.tj0 + ty;
     const bool active = i < a.box.hi[0] && j < a.box.hi[1];
-    live = active;
+    live = F || active;
     if (X) {  // this column's x/y halo layers (fused send)
       const int xm = a.xd->xmask;
       int mm = 0;
