@@ -136,7 +136,7 @@ class ClockSampler:
         if not self.proc or not self.path:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         with open(self.path) as fh:
             for line in fh:
                 parts = [x.strip() for x in line.split(",")]
@@ -147,6 +147,10 @@ class ClockSampler:
                     mx.append(float(parts[2]))
                 except ValueError:
                     continue
+                try:
+                    pw.append(float(parts[3]))
+                except ValueError:
+                    pass
                 for nm, val in zip(names, parts[4:8]):
                     if val.lower().startswith("active"):
                         reasons.add(nm)
@@ -154,8 +158,9 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm.sort()
+        pw.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "power_w": pw[len(pw) // 2] if pw else None}
 
 
 def ref_decomposition(grid, mode, max_np):
