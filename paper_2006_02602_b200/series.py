@@ -10,11 +10,12 @@ device = rank % visible GPUs) for `warmup` untimed and `steps` timed
 iterations (Block.bench: CUDA events on each rank's stream, max over
 ranks). Next to the reference's 12 columns a sidecar CSV carries what the
 reference cannot measure: the step kernel's fraction of the HBM roofline
-(80 B per cell-update), the time the compute stream waited for
-peers (scalars, then the halo join after the internal items) as a share of
-the iteration, and how many GPUs the ranks shared. With fewer GPUs than
-ranks the ranks' kernels share SMs, so those rows measure the multi-rank
-path's extra work, not scaling.
+(80 B per cell-update; per rank, so only when every rank has
+its own GPU), the whole iteration's fraction of the roofline of the GPUs
+used (hbm_frac_of_step), the time the compute stream waited for peers as a
+share of the iteration, and how many GPUs the ranks shared. With fewer GPUs
+than ranks the ranks' kernels share SMs, so those rows measure the
+multi-rank path's extra work, not scaling.
 """
 import json
 import os
@@ -24,7 +25,8 @@ from . import capi
 from .records import RunRecord, ScalingSeries, csv_text
 
 BYTES_PER_CELL = 80
-EXTRA_HEADER = "np,mode,dims,strategy,overlap,size,gpus,ms_per_step,step_kernel_ms,roofline_frac,exposed_comm_frac"
+EXTRA_HEADER = ("np,mode,dims,strategy,overlap,size,gpus,ms_per_step,step_kernel_ms,roofline_frac,hbm_frac_of_step,"
+                "exposed_comm_frac")
 
 
 def _peak():
@@ -109,10 +111,13 @@ def run_series(grid, np_list, modes, strategies=("v3",), scaling="strong", overl
                                 efficiency=float("nan"), bytes_sent=t["bytes_per_iteration"] * steps)
                 s.rows.append(rec)
                 ms = t["total_ms"] / steps
+                own_gpu = t["gpus"] >= np_
                 extra.append({"np": np_, "mode": mode, "dims": rec.dims, "strategy": strat,
                               "overlap": rec.overlap, "size": size, "gpus": t["gpus"], "ms_per_step": ms,
                               "step_kernel_ms": t["step_ms"],
-                              "roofline_frac": BYTES_PER_CELL * t["cells_max"] / (t["step_ms"] * 1e-3) / 1e9 / peak,
+                              "roofline_frac": (BYTES_PER_CELL * t["cells_max"] / (t["step_ms"] * 1e-3) / 1e9 / peak
+                                                if own_gpu else float("nan")),
+                              "hbm_frac_of_step": BYTES_PER_CELL * size / (ms * 1e-3) / 1e9 / (t["gpus"] * peak),
                               "exposed_comm_frac": t["wait_ms"] / ms if ms > 0 else float("nan")})
             if s.rows:
                 s.validate()
