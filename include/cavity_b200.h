@@ -299,10 +299,13 @@ typedef struct {
   int err_kind;             /* out: 0 repro_sum non-finite, 1..5 compute_dt field p,u,v,w,T */
   double seconds;           /* out: device time of iterations first_it+1.. (iteration 1 excluded when first_it==1) */
   cav_ledger ledger;        /* in/out: accumulated */
-  /* Device-side convergence (single-rank blocks; ignored otherwise): with
-   * device_conv and want_norms, the run stops on the device after the first
-   * check iteration where max_v |R_v| / peak_v <= conv_tol (the rule of
-   * src/runner.cpp:210-220); no iteration after it is marched. */
+  /* Device-side convergence: with device_conv and want_norms, the run stops
+   * on the device after the first check iteration where
+   * max_v |R_v| / peak_v <= conv_tol (the rule of src/runner.cpp:210-220);
+   * no iteration after it is marched. With several ranks every rank pushes
+   * its exact digits to every rank after each check and all decide on the
+   * merged sums, so every rank must pass the same device_conv, check_every
+   * and iteration range. */
   int device_conv;          /* in: request; out: 1 if this block honoured it (else all n_its were marched) */
   double conv_tol;          /* in */
   double conv_peaks[5];     /* in/out: per-variable peak norms carried across calls */
@@ -310,8 +313,10 @@ typedef struct {
 } cav_run_io;
 
 /* Marches n_its iterations of rank_main's loop body (src/runner.cpp:184-235)
- * on the device: BC, exchange (plan per strategy, optional overlap),
- * fused residual + [norms] + dt + Euler update + centre-pressure rescale.
+ * on the device: BC, exchange (plan per strategy; the step kernel stores the
+ * halos into the neighbours' states, or the slab exchange with optional
+ * overlap), fused residual + [norms] + dt + Euler update + centre-pressure
+ * rescale. One-rank runs replay pairs of plain iterations as CUDA graphs.
  * Synchronous. */
 int cav_block_run(cav_block* b, cav_run_io* io);
 /* Number of launches of this library's kernels per iteration (bench claim). */
@@ -324,9 +329,9 @@ int cav_block_scalars(cav_block* b, double* dt_out, double* pc_out);
 
 /* Bench hook: time n_its iterations with CUDA events on the block's compute
  * stream. out[0] total ms; out[1] fused-step kernel ms per iteration (both
- * launches when overlapping); out[2] ms per iteration the compute stream
- * spent waiting for peers (scalars, then the halo join): the exposed
- * communication. */
+ * launches when the slab exchange overlaps); out[2] ms per iteration the
+ * compute stream spent waiting for peers (their scalars, and with the slab
+ * exchange the halo join): the exposed communication. */
 int cav_block_bench(cav_block* b, long long n_its, double out[3]);
 
 #ifdef __cplusplus
