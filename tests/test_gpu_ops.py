@@ -161,3 +161,20 @@ def test_copy_box_index_maps(face, depth):
         lo, hi = box
         np.testing.assert_array_equal(back[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]],
                                       f[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]])
+
+
+@pytest.mark.parametrize("box", [((2, 2, 2), (2, 12, 11)), ((5, 3, 4), (11, 3, 8)), ((4, 4, 4), (3, 9, 9))])
+def test_empty_boxes_are_no_ops(box):
+    """residual_box / update_box on an empty box (some hi <= lo) write
+    nothing, as the reference's loops do (src/kernels_scalar.cpp:5-30)."""
+    n = (16, 10, 9)
+    f = O.random_fields(n, 5)
+    h = (0.05 / 15, 0.06 / 9, 0.045 / 8)
+    sp = capi.stencil_params(*h, fluid())
+    fin = [dev(f[v]) for v in range(5)]
+    out = [torch.full_like(x, 12345.0) for x in fin]
+    capi.residual_box(fin, out, n[0] + 4, n[1] + 4, box, sp)
+    assert all(bool((t == 12345.0).all()) for t in out)
+    q = dev(f[1])
+    capi.update_box(q, out[1], 0.25, n[0] + 4, n[1] + 4, box)
+    np.testing.assert_array_equal(bits(host(q)), bits(f[1]))
