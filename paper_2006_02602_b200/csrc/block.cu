@@ -1393,8 +1393,15 @@ void Block::iteration_pair_graph(long long it) {
   if (!gexec[key]) {  // capture once: the launches' arguments depend only on (cur, it & 1)
     cudaGraph_t gr = nullptr;
     CAV_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
-    iteration(it, false, nullptr, nullptr);
-    iteration(it + 1, false, nullptr, nullptr);
+    try {
+      iteration(it, false, nullptr, nullptr);
+      iteration(it + 1, false, nullptr, nullptr);
+    } catch (...) {  // leave the stream out of capture mode before reporting
+      cudaStreamEndCapture(s0, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      cudaGetLastError();
+      throw;
+    }
     CAV_CUDA(cudaStreamEndCapture(s0, &gr));
     const cudaError_t e = cudaGraphInstantiate(&gexec[key], gr, 0);
     cudaGraphDestroy(gr);
