@@ -280,3 +280,49 @@ def test_multi_rank_blocks_from_uploaded_state(monkeypatch, dims, strategy, fuse
     finally:
         for b in blocks:
             b.close()
+
+
+def test_cpp_host_runs_the_case_through_the_c_abi(tmp_path):
+    """The C++ host path north_star keeps: a g++-compiled driver includes
+    include/cavity_b200.hpp, links libcavity_b200.so and runs cases (one rank,
+    and two in-process ranks with fused halos); its fields and norm history
+    equal the oracle's bitwise."""
+    import shutil
+    import subprocess
+    import os
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    root = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+    src = tmp_path / "drv.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <cstdlib>
+#include "cavity_b200.hpp"
+int main(int argc, char** argv) {
+  cav_run_config c = cavity_b200::default_config();
+  c.nx = 24; c.ny = 20; c.nz = 16; c.steps = 60; c.check_every = 10;
+  c.np = std::atoi(argv[1]); c.mode = CAV_MODE_1D_K;
+  const cavity_b200::case_result r = cavity_b200::run_case(c, true, true);
+  FILE* f = std::fopen(argv[2], "wb");
+  std::fwrite(r.fields.data(), sizeof(double), r.fields.size(), f);
+  std::fwrite(r.history.data(), sizeof(double), r.history.size(), f);
+  std::fclose(f);
+  std::printf("%lld %zu\n", r.raw.steps_marched, r.history_iter.size());
+  return 0;
+}''')
+    exe = tmp_path / "drv"
+    lib_dir = os.path.dirname(capi.lib_path())
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"), str(src), "-L", lib_dir,
+                    "-lcavity_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    o = Oracle.run_case(capi.default_config(grid=(24, 20, 16), steps=60, check_every=10), collect_fields=True,
+                        collect_history=True)
+    for np_ in (1, 2):
+        out = tmp_path / f"r{np_}.bin"
+        p = subprocess.run([str(exe), str(np_), str(out)], capture_output=True, text=True, timeout=120,
+                           env=dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32"))
+        assert p.returncode == 0, p.stderr
+        assert p.stdout.split() == ["60", str(len(o["history_iter"]))]
+        data = np.fromfile(out, dtype=np.float64)
+        nf = o["fields"].size
+        np.testing.assert_array_equal(bits(data[:nf]), bits(o["fields"].ravel()))
+        np.testing.assert_array_equal(bits(data[nf:]), bits(o["history"].ravel()))
