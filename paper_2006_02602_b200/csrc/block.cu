@@ -382,8 +382,13 @@ struct ConvState {
 constexpr int kNormRunThreads = 256, kNormRunSeg = 128;
 static_assert(kNormRunSeg <= 4096, "a digit run of up to kNormRunSeg terms must fit its 96 bits");
 // One variable per thread (blockIdx.y = variable): a 96-bit run and a
-// running maximum are all the state a thread keeps (32 registers, full
-// occupancy); measured 2% faster per norm iteration than five per thread.
+// running maximum are all the state a thread keeps; measured 2% faster per
+// norm iteration than five per thread. A: planes loaded per batch before
+// their terms are summed (the digit runs' shared atomics keep the compiler
+// from hoisting later loads, so A = 1 has one load in flight per thread and
+// is latency-bound: ncu at 256^3, 220 us and 3.0 TB/s for A = 1, 124 us and
+// 5.4 TB/s for A = 8, 48 registers; CAV_NORM_AHEAD=1 selects the former).
+template <int A>
 __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs, Geo g, cav_box b,
                                                                unsigned long long* dig,
                                                                unsigned long long* err_sticky, long long n,
@@ -405,13 +410,17 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
     const long long plane = static_cast<long long>(g.pitch) * g.ypitch;
     const int k1 = min(k0 + kNormRunSeg, b.hi[2]);
     const double* q = rs + v * g.fstride + g.idx(i, j, k0);
-#pragma unroll 4
-    for (int k = k0; k < k1; ++k, q += plane) {
-      const double x = __ldcs(q);
-      mx = max(mx, abs_bits(x));
-      const double x2 = x * x;
-      if (nonfinite(x2)) nf = 1;
-      else digit_run_add(run, sd, x2);
+    for (int k = k0; k < k1; k += A, q += A * plane) {
+      double x[A];
+#pragma unroll
+      for (int u = 0; u < A; ++u) x[u] = k + u < k1 ? __ldcs(q + u * plane) : 0.0;  // 0: no term
+#pragma unroll
+      for (int u = 0; u < A; ++u) {
+        mx = max(mx, abs_bits(x[u]));
+        const double x2 = x[u] * x[u];
+        if (nonfinite(x2)) nf = 1;
+        else digit_run_add(run, sd, x2);
+      }
     }
     digit_run_flush(run, sd);
   }
@@ -426,12 +435,22 @@ __global__ void __launch_bounds__(kNormRunThreads) k_norm_runs(const double* rs,
   if (nf) atomicMin(err_sticky, err_code(n, rank, 0));  // the step kernel's non-finite norm error
 }
 
+int getenv_int(const char* name, int dflt);
+
+int norm_ahead() {
+  static const int a = getenv_int("CAV_NORM_AHEAD", 8);
+  return a;
+}
+
 void launch_norm_runs(const double* rs, const Geo& g, const cav_box& b, unsigned long long* dig,
                       unsigned long long* err, long long n, int rank, const int* stop, cudaStream_t st) {
   const long long cols = static_cast<long long>(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) *
                          ((b.hi[2] - b.lo[2] + kNormRunSeg - 1) / kNormRunSeg);
   const dim3 grid(static_cast<unsigned>((cols + kNormRunThreads - 1) / kNormRunThreads), 5);
-  k_norm_runs<<<grid, kNormRunThreads, 0, st>>>(rs, g, b, dig, err, n, rank, stop);
+  switch (norm_ahead()) {
+    case 1: k_norm_runs<1><<<grid, kNormRunThreads, 0, st>>>(rs, g, b, dig, err, n, rank, stop); break;
+    default: k_norm_runs<8><<<grid, kNormRunThreads, 0, st>>>(rs, g, b, dig, err, n, rank, stop); break;
+  }
   CAV_CUDA(cudaGetLastError());
 }
 
@@ -874,7 +893,7 @@ Block::Block(const cav_block_desc& desc) : d(desc) {
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_import));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_center_pcs));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_conv_check));
-    CAV_CUDA(cudaFuncGetAttributes(&fa, k_norm_runs));
+    CAV_CUDA(cudaFuncGetAttributes(&fa, k_norm_runs<8>));
     CAV_CUDA(cudaFuncGetAttributes(&fa, k_ghosts_yz));
   }
   {
