@@ -99,7 +99,9 @@ def step_traffic():
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    # power.draw.instant: power.draw is a 1 s average and lags a sub-second
+    # timed region (a 2000-step 256^3 run read ~510 W while drawing ~995 W)
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -108,13 +110,23 @@ class ClockSampler:
         self.proc = None
         self.path = None
 
+    def _fields(self):
+        try:  # older drivers lack power.draw.instant: fall back to the averaged reading
+            r = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=power.draw.instant",
+                               "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+            float(r.stdout.strip().splitlines()[0])
+            return self.FIELDS
+        except Exception:
+            return self.FIELDS.replace("power.draw.instant", "power.draw")
+
     def __enter__(self):
         try:
+            fields = self._fields()
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + fields,
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
             time.sleep(0.3)

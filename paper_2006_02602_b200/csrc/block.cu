@@ -580,7 +580,16 @@ CUtensorMap make_state_map(const double* base, const Geo& g, int nfields, int bw
 // The step configuration: 32 x 8 tiles (8 consumer warps + 1 TMA issuer warp),
 // a 7-slot ring, 2 CTAs per SM. The measured alternatives (other tile
 // heights, ring depths, 1 CTA per SM) are listed in DESIGN.md §3.
-using TmaV0 = TmaCfg<8, 7, 2>;
+#ifndef CAV_TMA_TY  // variant builds (scripts/build_variant.sh): -DCAV_TMA_TY=.. -DCAV_TMA_R=.. -DCAV_TMA_CTAS=..
+#define CAV_TMA_TY 8
+#endif
+#ifndef CAV_TMA_R
+#define CAV_TMA_R 7
+#endif
+#ifndef CAV_TMA_CTAS
+#define CAV_TMA_CTAS 2
+#endif
+using TmaV0 = TmaCfg<CAV_TMA_TY, CAV_TMA_R, CAV_TMA_CTAS>;
 constexpr int kTY = TmaV0::TY;
 
 template <class Cfg, bool NORMS, bool G, bool X>
