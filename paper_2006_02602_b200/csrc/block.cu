@@ -486,6 +486,36 @@ __global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz(double* s, Geo g, W
   }
 }
 
+// Even nx: two neighbouring columns per thread with 16-byte loads and stores
+// (rows start 128-byte aligned at i = 2), the same expressions as k_ghosts_yz.
+__global__ void __launch_bounds__(kGhostThreads) k_ghosts_yz2(double* s, Geo g, WallInfo w, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  const int face = 2 + static_cast<int>(blockIdx.z);
+  if (!w.wall[face]) return;
+  const int ax = face >> 1, hi = face & 1;
+  const int nn = ax == 1 ? g.ny : g.nz, nt = ax == 1 ? g.nz : g.ny;
+  if (static_cast<int>(blockIdx.y) >= nt) return;
+  const int t = 2 + static_cast<int>(blockIdx.y);
+  const int c0 = hi ? nn + 1 : 2, c1 = hi ? nn : 3, c2 = hi ? nn - 1 : 4, g0 = hi ? nn + 2 : 1, g1 = hi ? nn + 3 : 0;
+  const long long fs = g.fstride;
+  for (int i = 2 + 2 * (static_cast<int>(blockIdx.x) * kGhostThreads + static_cast<int>(threadIdx.x)); i < g.nx + 2;
+       i += 2 * static_cast<int>(gridDim.x) * kGhostThreads) {
+    auto at = [&](int nrm) { return ax == 1 ? g.idx(i, nrm, t) : g.idx(i, t, nrm); };
+    auto ld = [&](long long e) { return *reinterpret_cast<const double2*>(s + e); };
+    auto st2 = [&](long long e, double a, double b) { *reinterpret_cast<double2*>(s + e) = make_double2(a, b); };
+    const long long e0 = at(c0), q0 = at(g0);
+    const double2 p0 = ld(e0), p1 = ld(at(c1)), p2 = ld(at(c2));
+    const double2 u = ld(fs + e0), v = ld(2 * fs + e0), wv = ld(3 * fs + e0), tt = ld(4 * fs + e0);
+    const double ga = cubic_g0(p0.x, p1.x, p2.x), gb = cubic_g0(p0.y, p1.y, p2.y);
+    st2(q0, ga, gb);
+    st2(at(g1), cubic_g1(ga, p0.x, p1.x), cubic_g1(gb, p0.y, p1.y));
+    st2(fs + q0, -u.x, -u.y);  // no-slip: antisymmetric velocity
+    st2(2 * fs + q0, -v.x, -v.y);
+    st2(3 * fs + q0, -wv.x, -wv.y);
+    st2(4 * fs + q0, tt.x, tt.y);  // adiabatic
+  }
+}
+
 __global__ void k_conv_check(const unsigned long long* dig, ConvState* c, long long it, double tol, double nglobal,
                              const NormSlot* merge, int np, int par, unsigned long long stamp, const int* abort) {
   if (c->stop) return;
@@ -1307,9 +1337,15 @@ void Block::launch_ghosts() {
   // wall ghosts of the output state for the next step (no pending shift)
   if (step_wrote_ghosts) {
     if (!(walls[2] || walls[3] || walls[4] || walls[5])) return;
-    const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
-    k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo,
-                                                d.np == 1 ? &conv->stop : (stop_flag ? stop_flag : abort_flag));
+    const int* stp = d.np == 1 ? &conv->stop : (stop_flag ? stop_flag : abort_flag);
+    static const bool pairs = getenv_int("CAV_GHOST_PAIRS", 1) != 0;
+    if (pairs && n[0] % 2 == 0) {
+      const dim3 grid((n[0] / 2 + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
+      k_ghosts_yz2<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo, stp);
+    } else {
+      const dim3 grid((n[0] + kGhostThreads - 1) / kGhostThreads, std::max(n[1], n[2]), 4);
+      k_ghosts_yz<<<grid, kGhostThreads, 0, s0>>>(state[cur ^ 1], g, winfo, stp);
+    }
     CAV_CUDA(cudaGetLastError());
   } else {
     double* fo[5] = {field(cur ^ 1, 0), field(cur ^ 1, 1), field(cur ^ 1, 2), field(cur ^ 1, 3), field(cur ^ 1, 4)};
