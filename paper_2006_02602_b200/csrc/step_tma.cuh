@@ -145,15 +145,7 @@ struct TmaCfg {
   static constexpr int QField = kQW * QH;     // doubles per u/v/w/T part
   static constexpr int Slot = PField + 4 * QField;
   static constexpr int TxBytes = (kPW * PH + 4 * QField) * 8;  // bytes the two boxes deliver
-#if CAV_SETMAXNREG
-  // variant (-DCAV_SETMAXNREG=1 -DCAV_SETMAXNREG_HI=104 -DCAV_SETMAXNREG_LO=24):
-  // a whole issuer warpgroup (4 warps, 3 idle) at LO registers, consumers at
-  // HI instead of 96 (the CTA pool is 384 x 80); measured -1%
-  static_assert(TY % 4 == 0, "consumer warps must form whole warpgroups");
-  static constexpr int Threads = 32 * (TY + 4);
-#else
   static constexpr int Threads = 32 * (TY + 1);  // consumers + issuer
-#endif
   static constexpr int NC = 32 * TY;              // consumer threads
   static constexpr size_t Smem = static_cast<size_t>(R) * Slot * sizeof(double) + 3 * R * 8 + (5 * kDigits + 8) * 8;
   static_assert(PField * 8 % 128 == 0 && Slot * 8 % 128 == 0, "TMA destinations must stay 128-byte aligned");
@@ -676,14 +668,6 @@ __global__ void __launch_bounds__(Cfg::Threads, Cfg::CTAS)
 
   const long long total = static_cast<long long>(a.ntiles) * a.nchunks;
 
-#if CAV_SETMAXNREG
-  if (warp >= C) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CAV_SETMAXNREG_LO));
-    if (warp != C) return;
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CAV_SETMAXNREG_HI));
-  }
-#endif
   if (warp == C) {
     // ---------------- TMA issuer (one lane) ----------------
     if (lane != 0) return;
